@@ -1,0 +1,786 @@
+// engine.cu — the SubNetAct execution engine behind the C-ABI of include/ssn.h.
+//
+// What replaces the reference's mock worker (serve_runtime.hpp:161-172):
+//  * weight store   — every max-shape conv/linear tensor uploaded ONCE
+//                     (layers "shared in place");
+//  * SubnetNorm     — per registered subnet, (gamma, beta, mu_ij, var_ij) folded
+//                     into a scale/shift row;
+//  * WeightSlice    — per-subnet OpDesc rows give every kernel its active
+//                     extents; kernels read leading slices of the store;
+//  * LayerSelect    — per (segment, depth-variant, batch) CUDA graphs built in
+//                     ssn_prepare(); a forward launches only the variants whose
+//                     blocks the subnet runs;
+//  * actuation      — ssn_actuate(id) re-points one device word at the
+//                     subnet's OpDesc row (one 1-thread kernel at the next
+//                     forward); no weight moves.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ssn.h"
+#include "../../include/ssn_rng.h"
+#include "device.cuh"
+#include "supernet.hpp"
+
+namespace ssn {
+int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int bn);
+int choose_bn(int cout_max, long M);
+cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& map, cudaStream_t s);
+cudaError_t init_conv_tc();
+cudaError_t launch_input(const InputParams& p, cudaStream_t s);
+cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
+cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
+cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
+}  // namespace ssn
+
+using namespace ssn;
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_last_error;
+
+struct SsnError {
+  int code;
+  std::string msg;
+};
+
+#define SSN_THROW(code, msg) throw SsnError{code, msg}
+#define CUDA_TRY(expr)                                                          \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess)                                                      \
+      SSN_THROW(SSN_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return SSN_OK;
+  } catch (const SsnError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return SSN_E_INVALID;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return SSN_E_RANGE;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return SSN_E_NOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SSN_E_INVALID;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// engine
+
+static constexpr int NBUF = 6;  // BND0, BND1, P, T1, T2, T3
+enum { B_BND0 = 0, B_BND1 = 1, B_P = 2, B_T1 = 3, B_T2 = 4, B_T3 = 5 };
+
+struct SubnetState {
+  bool ok = false;
+  Net plan;
+  OpDesc* d_row = nullptr;
+  float* d_norm = nullptr;
+  uint64_t norm_bytes = 0;
+  uint64_t stat_bytes = 0;
+  std::vector<uint32_t> seg_mask;
+};
+
+struct ssn_engine {
+  int device = 0;
+  ssn_supernet_desc desc{};
+  Net net;  // max-shape plan
+  bool bf16 = true;
+  uint8_t* d_w = nullptr;
+  std::vector<std::vector<float>> gamma, beta;  // host copies for SubnetNorm folding
+  std::vector<CUtensorMap> tmaps;  // per op (tcgen05 convs)
+  std::vector<int> op_bn;
+  std::vector<SubnetState> subs;
+  const OpDesc** d_rowptr = nullptr;
+  int active = -1;
+  bool dirty = false;
+  void* bufs[NBUF] = {};
+  size_t buf_bytes = 0;
+  void* d_raw = nullptr;
+  size_t raw_img_bytes = 0;
+  float* d_logits = nullptr;
+  std::vector<uint32_t> grid;
+  std::map<uint64_t, std::pair<cudaGraphExec_t, int>> graphs;  // key -> (exec, kernels)
+  cudaStream_t stream = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  double last_actuate_us = 0, last_forward_host_us = 0;
+  uint32_t last_kernels = 0, last_graphs = 0;
+  bool prepared = false;
+};
+
+static uint64_t graph_key(int seg, uint32_t mask, uint32_t batch) {
+  return (static_cast<uint64_t>(seg) << 48) | (static_cast<uint64_t>(mask) << 32) | batch;
+}
+
+static size_t raw_image_bytes(const ssn_supernet_desc& d) {
+  const size_t px = static_cast<size_t>(d.image_size) * d.image_size;
+  return d.input_format == SSN_INPUT_U8_NHWC ? px * 3 : px * 3 * 4;
+}
+
+static void validate_desc(const ssn_supernet_desc* d) {
+  if (!d) SSN_THROW(SSN_E_INVALID, "null supernet descriptor");
+  if (d->family != SSN_FAMILY_TINYCNN && d->family != SSN_FAMILY_OFA_RESNET50)
+    SSN_THROW(SSN_E_INVALID, "unsupported supernet family " + std::to_string(d->family));
+  if (d->dtype != SSN_DTYPE_F32 && d->dtype != SSN_DTYPE_BF16)
+    SSN_THROW(SSN_E_INVALID, "dtype must be SSN_DTYPE_F32 or SSN_DTYPE_BF16");
+  if (d->image_size < 8 || d->image_size > 1024) SSN_THROW(SSN_E_INVALID, "image_size out of range");
+  if (d->num_classes < 1 || d->num_classes > 100000) SSN_THROW(SSN_E_INVALID, "num_classes out of range");
+  if (d->max_batch < 1) SSN_THROW(SSN_E_INVALID, "max_batch must be >= 1");
+  if (d->input_format > SSN_INPUT_U8_NHWC) SSN_THROW(SSN_E_INVALID, "bad input_format");
+}
+
+// Fill a blob following DESIGN.md §4 from the ssn_rng.h specification.
+static void generate_blob(const Net& net, uint8_t* blob) {
+  const uint64_t seed = net.desc.seed;
+  const bool bf16 = net.elem_bytes == 2;
+  std::memset(blob, 0, net.blob_bytes);
+  for (size_t ti = 0; ti < net.tensors.size(); ++ti) {
+    const TensorSpec& t = net.tensors[ti];
+    const int kk = t.k * t.k;
+    for (int o = 0; o < t.cout; ++o)
+      for (int i = 0; i < t.cin; ++i)
+        for (int r = 0; r < t.k; ++r)
+          for (int s = 0; s < t.k; ++s) {
+            const uint64_t idx = ((static_cast<uint64_t>(o) * t.cin + i) * t.k + r) * t.k + s;
+            const float v = ssn_weight_value(seed, static_cast<uint32_t>(ti), idx, t.fan_in, bf16);
+            // storage: KRSC [cout][k][k][cin_store] (depthwise: [c][k][k])
+            const uint64_t e = (static_cast<uint64_t>(o) * kk + r * t.k + s) * t.cin_store + i;
+            if (bf16) {
+              reinterpret_cast<uint16_t*>(blob + t.w_off)[e] = ssn_f32_to_bf16_bits(v);
+            } else {
+              reinterpret_cast<float*>(blob + t.w_off)[e] = v;
+            }
+          }
+    if (t.linear)
+      for (int o = 0; o < t.cout; ++o)
+        reinterpret_cast<float*>(blob + t.b_off)[o] =
+            ssn_bias_value(seed, static_cast<uint32_t>(ti), o);
+  }
+  for (size_t ni = 0; ni < net.norms.size(); ++ni) {
+    const NormSpec& n = net.norms[ni];
+    for (int c = 0; c < n.c; ++c) {
+      reinterpret_cast<float*>(blob + n.gamma_off)[c] =
+          n.res ? ssn_gamma_res_value(seed, static_cast<uint32_t>(ni), c)
+                : ssn_gamma_value(seed, static_cast<uint32_t>(ni), c);
+      reinterpret_cast<float*>(blob + n.beta_off)[c] =
+          ssn_beta_value(seed, static_cast<uint32_t>(ni), c);
+    }
+  }
+}
+
+static void* slot_ptr(ssn_engine* e, int slot, const int* map) {
+  switch (slot) {
+    case S_NONE: return nullptr;
+    case S_RAW: return e->d_raw;
+    case S_LOGITS: return e->d_logits;
+    default: return e->bufs[map[slot]];
+  }
+}
+
+// Enqueue one op (called under stream capture).
+static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cudaStream_t s) {
+  const OpSpec& o = e->net.ops[oi];
+  const bool bf = e->bf16;
+  switch (o.kind) {
+    case OP_INPUT: {
+      InputParams p{};
+      p.raw = e->d_raw;
+      p.y = slot_ptr(e, o.out, map);
+      p.n = static_cast<int>(batch);
+      p.h = o.hin;
+      p.w = o.win;
+      p.format = static_cast<int>(e->desc.input_format);
+      p.cpad = o.cout_max;
+      p.out_bf16 = bf;
+      CUDA_TRY(launch_input(p, s));
+      return 1;
+    }
+    case OP_MAXPOOL:
+    case OP_AVGPOOL:
+    case OP_GAP: {
+      PoolParams p{};
+      p.x = slot_ptr(e, o.in, map);
+      p.y = slot_ptr(e, o.out, map);
+      p.row = e->d_rowptr;
+      p.op = oi;
+      p.n = static_cast<int>(batch);
+      p.h = o.hin;
+      p.w = o.win;
+      p.ho = o.hout;
+      p.wo = o.wout;
+      p.k = o.kind == OP_AVGPOOL ? o.pool_k : o.k_max;
+      p.stride = o.kind == OP_AVGPOOL ? o.pool_k : o.stride;
+      p.pad = o.kind == OP_MAXPOOL ? 1 : 0;
+      p.kind = o.kind == OP_MAXPOOL ? 2 : (o.kind == OP_AVGPOOL ? 3 : 4);
+      CUDA_TRY(launch_pool(p, o.cin_max, bf, s));
+      return 1;
+    }
+    case OP_CONV:
+    case OP_LINEAR: {
+      const TensorSpec& t = e->net.tensors[o.tensor];
+      ConvParams p{};
+      p.x = slot_ptr(e, o.in, map);
+      p.y = slot_ptr(e, o.out, map);
+      p.res = slot_ptr(e, o.res, map);
+      p.w = e->d_w + t.w_off;
+      p.row = e->d_rowptr;
+      p.fixed = nullptr;
+      p.op = oi;
+      p.n = static_cast<int>(batch);
+      p.h = o.hin;
+      p.w_ = o.win;
+      p.ho = o.hout;
+      p.wo = o.wout;
+      p.stride = o.stride;
+      p.M = static_cast<int>(batch) * o.hout * o.wout;
+      p.k_max = o.k_max;
+      p.cin_max = t.cin_store;
+      p.cout_max = o.cout_max;
+      p.act = o.act;
+      p.res_post = o.res_post;
+      p.out_f32 = o.kind == OP_LINEAR;
+      p.depthwise = o.depthwise;
+      if (bf && !o.depthwise) {
+        p.bn = choose_bn(o.cout_max, p.M);
+        CUtensorMap map_{};
+        if (make_weight_map(&map_, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
+        CUDA_TRY(launch_conv_tc(p, map_, s));
+      } else {
+        if (bf) SSN_THROW(SSN_E_INVALID, "bf16 depthwise conv not supported for this family");
+        CUDA_TRY(launch_conv_f32(p, s));
+      }
+      return 1;
+    }
+  }
+  SSN_THROW(SSN_E_INVALID, "unknown op kind");
+}
+
+// Capture the graph of segment `seg` for LayerSelect variant `mask` at `batch`.
+static void build_graph(ssn_engine* e, int seg, uint32_t mask, uint32_t batch) {
+  const SegmentSpec& S = e->net.segments[seg];
+  std::vector<int> act;
+  for (int bi : S.blocks) {
+    const BlockSpec& b = e->net.blocks[bi];
+    bool on = b.flag < 0;
+    if (!on) {
+      for (size_t f = 0; f < S.flags.size(); ++f)
+        if (S.flags[f] == b.flag) on = (mask >> f) & 1u;
+    }
+    if (on) act.push_back(bi);
+  }
+  const int in_bnd = seg % 2 == 0 ? B_BND0 : B_BND1;
+  const int out_bnd = seg % 2 == 0 ? B_BND1 : B_BND0;
+  const int k = static_cast<int>(act.size());
+  int cur_in = in_bnd;
+  int kernels = 0;
+  CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int i = 0; i < k; ++i) {
+      const int out_buf = ((k - 1 - i) % 2 == 0) ? out_bnd : B_P;
+      int map[5];
+      map[S_IN] = cur_in;
+      map[S_OUT] = out_buf;
+      map[S_T1] = B_T1;
+      map[S_T2] = B_T2;
+      map[S_T3] = B_T3;
+      const BlockSpec& b = e->net.blocks[act[i]];
+      for (int q = 0; q < b.count; ++q) kernels += enqueue_op(e, b.first + q, map, batch, e->cap_stream);
+      cur_in = out_buf;
+    }
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(e->cap_stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamEndCapture(e->cap_stream, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(err);
+  e->graphs[graph_key(seg, mask, batch)] = {ex, kernels};
+}
+
+static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
+                            const float* mean, const float* var) {
+  if (!c) SSN_THROW(SSN_E_INVALID, "null subnet config");
+  if (id > 65535) SSN_THROW(SSN_E_RANGE, "subnet id must be < 65536");
+  SubnetCfg cfg = SubnetCfg::from_c(c);
+  Net plan = build_net(e->desc, &cfg);  // throws invalid_argument like SubnetConfig::validate
+  if (plan.ops.size() != e->net.ops.size()) SSN_THROW(SSN_E_STATE, "plan/op mismatch");
+  // SubnetNorm: fold shared gamma/beta with this subnet's (mu, var).
+  std::vector<float> norm;
+  std::vector<int64_t> norm_off(plan.ops.size(), -1);
+  for (size_t oi = 0; oi < plan.ops.size(); ++oi) {
+    const OpSpec& o = plan.ops[oi];
+    if (!o.active || o.norm < 0) continue;
+    norm_off[oi] = static_cast<int64_t>(norm.size());
+    const auto& g = e->gamma[o.norm];
+    const auto& b = e->beta[o.norm];
+    std::vector<float> sc(o.cout), sh(o.cout);
+    for (int ch = 0; ch < o.cout; ++ch) {
+      const float mu = mean ? mean[o.stat_off + ch]
+                            : ssn_stat_mean_value(e->desc.seed, id, o.norm_slot, ch);
+      const float vr = var ? var[o.stat_off + ch]
+                           : ssn_stat_var_value(e->desc.seed, id, o.norm_slot, ch);
+      if (!(vr >= 0.f)) SSN_THROW(SSN_E_INVALID, "SubnetNorm variance must be >= 0");
+      const float inv = 1.0f / std::sqrt(vr + 1e-5f);
+      sc[ch] = g[ch] * inv;
+      sh[ch] = b[ch] - mu * sc[ch];
+    }
+    norm.insert(norm.end(), sc.begin(), sc.end());
+    norm.insert(norm.end(), sh.begin(), sh.end());
+  }
+  SubnetState st;
+  st.plan = std::move(plan);
+  st.norm_bytes = norm.size() * sizeof(float);
+  st.stat_bytes = st.plan.stat_count * 2 * sizeof(float);
+  if (!norm.empty()) {
+    CUDA_TRY(cudaMalloc(&st.d_norm, st.norm_bytes));
+    CUDA_TRY(cudaMemcpy(st.d_norm, norm.data(), st.norm_bytes, cudaMemcpyHostToDevice));
+  }
+  std::vector<OpDesc> row(st.plan.ops.size());
+  for (size_t oi = 0; oi < st.plan.ops.size(); ++oi) {
+    const OpSpec& o = st.plan.ops[oi];
+    OpDesc& dsc = row[oi];
+    dsc.cin = o.cin;
+    dsc.cout = o.cout;
+    dsc.k = o.k;
+    dsc.pad = o.k / 2;
+    dsc.scale = nullptr;
+    dsc.shift = nullptr;
+    if (norm_off[oi] >= 0) {
+      dsc.scale = st.d_norm + norm_off[oi];
+      dsc.shift = st.d_norm + norm_off[oi] + o.cout;
+    }
+    if (o.kind == OP_LINEAR)
+      dsc.shift = reinterpret_cast<const float*>(e->d_w + e->net.tensors[o.tensor].b_off);
+  }
+  CUDA_TRY(cudaMalloc(&st.d_row, row.size() * sizeof(OpDesc)));
+  CUDA_TRY(cudaMemcpy(st.d_row, row.data(), row.size() * sizeof(OpDesc), cudaMemcpyHostToDevice));
+  st.seg_mask.assign(e->net.segments.size(), 0);
+  for (size_t si = 0; si < e->net.segments.size(); ++si)
+    for (size_t f = 0; f < e->net.segments[si].flags.size(); ++f)
+      if (cfg.depth[e->net.segments[si].flags[f]]) st.seg_mask[si] |= 1u << f;
+  st.ok = true;
+  if (id >= e->subs.size()) e->subs.resize(id + 1);
+  SubnetState& old = e->subs[id];
+  if (old.ok) {
+    // Re-registration: the previous row may be referenced by in-flight work.
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(old.d_row);
+    cudaFree(old.d_norm);
+    if (e->active == static_cast<int>(id)) e->dirty = true;
+  }
+  e->subs[id] = std::move(st);
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+
+extern "C" {
+
+const char* ssn_last_error(void) { return g_last_error.c_str(); }
+
+int ssn_weight_blob_bytes(const ssn_supernet_desc* desc, uint64_t* bytes) {
+  return guarded([&] {
+    validate_desc(desc);
+    if (!bytes) SSN_THROW(SSN_E_INVALID, "null output");
+    *bytes = build_net(*desc, nullptr).blob_bytes;
+  });
+}
+
+int ssn_generate_weight_blob(const ssn_supernet_desc* desc, void* blob, uint64_t bytes) {
+  return guarded([&] {
+    validate_desc(desc);
+    Net net = build_net(*desc, nullptr);
+    if (!blob || bytes < net.blob_bytes) SSN_THROW(SSN_E_INVALID, "blob too small");
+    generate_blob(net, static_cast<uint8_t*>(blob));
+  });
+}
+
+int ssn_plan_stat_count(const ssn_supernet_desc* desc, const ssn_subnet_cfg* c, uint64_t* count) {
+  return guarded([&] {
+    validate_desc(desc);
+    if (!c || !count) SSN_THROW(SSN_E_INVALID, "null argument");
+    SubnetCfg cfg = SubnetCfg::from_c(c);
+    *count = build_net(*desc, &cfg).stat_count;
+  });
+}
+
+int ssn_plan_ops(const ssn_supernet_desc* desc, const ssn_subnet_cfg* c, ssn_op_info* out,
+                 uint32_t capacity, uint32_t* n_ops) {
+  return guarded([&] {
+    validate_desc(desc);
+    if (!c || !n_ops) SSN_THROW(SSN_E_INVALID, "null argument");
+    SubnetCfg cfg = SubnetCfg::from_c(c);
+    Net net = build_net(*desc, &cfg);
+    *n_ops = static_cast<uint32_t>(net.ops.size());
+    if (!out) return;
+    if (capacity < net.ops.size()) SSN_THROW(SSN_E_RANGE, "op info capacity too small");
+    std::vector<int> blk(net.ops.size(), -1);
+    for (size_t bi = 0; bi < net.blocks.size(); ++bi)
+      for (int q = 0; q < net.blocks[bi].count; ++q) blk[net.blocks[bi].first + q] = static_cast<int>(bi);
+    for (size_t i = 0; i < net.ops.size(); ++i) {
+      const OpSpec& o = net.ops[i];
+      ssn_op_info& r = out[i];
+      r.kind = static_cast<uint32_t>(o.kind);
+      r.active = o.active;
+      r.k = static_cast<uint32_t>(o.kind == OP_AVGPOOL ? o.pool_k : o.k);
+      r.stride = static_cast<uint32_t>(o.stride);
+      r.hin = o.hin; r.win = o.win; r.hout = o.hout; r.wout = o.wout;
+      r.cin = o.cin; r.cout = o.cout; r.cin_max = o.cin_max; r.cout_max = o.cout_max;
+      r.depthwise = o.depthwise;
+      r.block = static_cast<uint32_t>(blk[i]);
+      r.segment = static_cast<uint32_t>(net.blocks[blk[i]].segment);
+      r.has_residual = o.res != S_NONE;
+    }
+  });
+}
+
+int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weights,
+               uint64_t host_weight_bytes, ssn_engine** out) {
+  return guarded([&] {
+    validate_desc(desc);
+    if (!out) SSN_THROW(SSN_E_INVALID, "null output handle");
+    *out = nullptr;
+    std::unique_ptr<ssn_engine> e(new ssn_engine());
+    e->device = device;
+    e->desc = *desc;
+    e->bf16 = desc->dtype == SSN_DTYPE_BF16;
+    e->net = build_net(*desc, nullptr);
+    CUDA_TRY(cudaSetDevice(device));
+    int major = 0, minor = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (e->bf16 && major != 10)
+      SSN_THROW(SSN_E_CUDA, "bf16 tcgen05 path requires an sm_100 (B200) device");
+    if (e->bf16) CUDA_TRY(init_conv_tc());
+    std::vector<uint8_t> gen;
+    const uint8_t* blob = static_cast<const uint8_t*>(host_weights);
+    if (!blob) {
+      gen.resize(e->net.blob_bytes);
+      generate_blob(e->net, gen.data());
+      blob = gen.data();
+    } else if (host_weight_bytes < e->net.blob_bytes) {
+      SSN_THROW(SSN_E_INVALID, "host weight blob too small: need " +
+                                   std::to_string(e->net.blob_bytes) + " bytes");
+    }
+    // weight store: uploaded once, shared in place by every subnet
+    CUDA_TRY(cudaMalloc(&e->d_w, e->net.blob_bytes));
+    CUDA_TRY(cudaMemcpy(e->d_w, blob, e->net.blob_bytes, cudaMemcpyHostToDevice));
+    for (const NormSpec& n : e->net.norms) {
+      const float* g = reinterpret_cast<const float*>(blob + n.gamma_off);
+      const float* b = reinterpret_cast<const float*>(blob + n.beta_off);
+      e->gamma.emplace_back(g, g + n.c);
+      e->beta.emplace_back(b, b + n.c);
+    }
+    // activation arena for the largest batch at max widths
+    size_t max_elems = 0;
+    for (const OpSpec& o : e->net.ops)
+      max_elems = std::max(max_elems, static_cast<size_t>(o.hout) * o.wout * o.cout_max);
+    e->buf_bytes = max_elems * desc->max_batch * (e->bf16 ? 2 : 4);
+    for (int i = 0; i < NBUF; ++i) CUDA_TRY(cudaMalloc(&e->bufs[i], e->buf_bytes));
+    e->raw_img_bytes = raw_image_bytes(*desc);
+    CUDA_TRY(cudaMalloc(&e->d_raw, e->raw_img_bytes * desc->max_batch));
+    CUDA_TRY(cudaMemset(e->d_raw, 0, e->raw_img_bytes * desc->max_batch));
+    CUDA_TRY(cudaMalloc(&e->d_logits, static_cast<size_t>(desc->max_batch) * desc->num_classes * 4));
+    CUDA_TRY(cudaMalloc(&e->d_rowptr, sizeof(OpDesc*)));
+    CUDA_TRY(cudaMemset(e->d_rowptr, 0, sizeof(OpDesc*)));
+    CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+    *out = e.release();
+  });
+}
+
+void ssn_destroy(ssn_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second.first);
+  for (auto& s : e->subs) {
+    cudaFree(s.d_row);
+    cudaFree(s.d_norm);
+  }
+  for (int i = 0; i < NBUF; ++i) cudaFree(e->bufs[i]);
+  cudaFree(e->d_raw);
+  cudaFree(e->d_logits);
+  cudaFree(e->d_rowptr);
+  cudaFree(e->d_w);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  delete e;
+}
+
+int ssn_subnet_stat_count(ssn_engine* e, const ssn_subnet_cfg* c, uint64_t* count) {
+  return guarded([&] {
+    if (!e || !c || !count) SSN_THROW(SSN_E_INVALID, "null argument");
+    SubnetCfg cfg = SubnetCfg::from_c(c);
+    *count = build_net(e->desc, &cfg).stat_count;
+  });
+}
+
+int ssn_register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c, const float* mean,
+                        const float* var) {
+  return guarded([&] {
+    if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    register_subnet(e, id, c, mean, var);
+  });
+}
+
+int ssn_prepare(ssn_engine* e, const uint32_t* batch_grid, uint32_t n) {
+  return guarded([&] {
+    if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    if (!batch_grid || n == 0) SSN_THROW(SSN_E_INVALID, "empty batch grid");
+    CUDA_TRY(cudaSetDevice(e->device));
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t b = batch_grid[i];
+      if (b == 0 || b > e->desc.max_batch)
+        SSN_THROW(SSN_E_RANGE, "batch " + std::to_string(b) + " outside [1, max_batch]");
+      if (i > 0 && b <= batch_grid[i - 1]) SSN_THROW(SSN_E_INVALID, "batch sizes must increase");
+    }
+    // A fixed row for capture-time validity (kernels only read it at replay).
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t b = batch_grid[i];
+      if (std::find(e->grid.begin(), e->grid.end(), b) != e->grid.end()) continue;
+      for (size_t si = 0; si < e->net.segments.size(); ++si) {
+        const uint32_t variants = 1u << e->net.segments[si].flags.size();
+        for (uint32_t m = 0; m < variants; ++m) build_graph(e, static_cast<int>(si), m, b);
+      }
+      e->grid.push_back(b);
+    }
+    std::sort(e->grid.begin(), e->grid.end());
+    e->prepared = true;
+  });
+}
+
+int ssn_actuate(ssn_engine* e, uint32_t id) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = guarded([&] {
+    if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    if (id >= e->subs.size() || !e->subs[id].ok)
+      SSN_THROW(SSN_E_RANGE, "subnet " + std::to_string(id) + " is not registered");
+    if (e->active != static_cast<int>(id)) {
+      e->active = static_cast<int>(id);
+      e->dirty = true;
+    }
+  });
+  if (e)
+    e->last_actuate_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_batch,
+                float* logits, void* stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = guarded([&] {
+    if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    if (e->active < 0) SSN_THROW(SSN_E_STATE, "no subnet actuated");
+    if (!e->prepared) SSN_THROW(SSN_E_STATE, "ssn_prepare() has not been called");
+    if (count == 0 || count > profiled_batch)
+      SSN_THROW(SSN_E_INVALID, "count must be in [1, profiled_batch]");
+    if (std::find(e->grid.begin(), e->grid.end(), profiled_batch) == e->grid.end())
+      SSN_THROW(SSN_E_RANGE, "batch size " + std::to_string(profiled_batch) + " not prepared");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+    const SubnetState& sub = e->subs[e->active];
+    uint32_t kernels = 0, graphs = 0;
+    if (e->dirty) {
+      CUDA_TRY(launch_set_row(e->d_rowptr, sub.d_row, s));
+      e->dirty = false;
+      ++kernels;
+    }
+    if (x) CUDA_TRY(cudaMemcpyAsync(e->d_raw, x, e->raw_img_bytes * count, cudaMemcpyDefault, s));
+    for (size_t si = 0; si < e->net.segments.size(); ++si) {
+      auto it = e->graphs.find(graph_key(static_cast<int>(si), sub.seg_mask[si], profiled_batch));
+      if (it == e->graphs.end()) SSN_THROW(SSN_E_STATE, "missing graph segment");
+      CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+      kernels += static_cast<uint32_t>(it->second.second);
+      ++graphs;
+    }
+    if (logits)
+      CUDA_TRY(cudaMemcpyAsync(logits, e->d_logits,
+                               static_cast<size_t>(count) * e->desc.num_classes * 4,
+                               cudaMemcpyDefault, s));
+    e->last_kernels = kernels;
+    e->last_graphs = graphs;
+  });
+  if (e)
+    e->last_forward_host_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+int ssn_synchronize(ssn_engine* e, void* stream) {
+  return guarded([&] {
+    if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    CUDA_TRY(cudaStreamSynchronize(stream ? static_cast<cudaStream_t>(stream) : e->stream));
+  });
+}
+
+int ssn_profile_latency(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t iters,
+                        double* median_us) {
+  return guarded([&] {
+    if (!e || !median_us || iters == 0) SSN_THROW(SSN_E_INVALID, "bad arguments");
+    if (ssn_actuate(e, id) != SSN_OK) SSN_THROW(SSN_E_RANGE, g_last_error);
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    for (int w = 0; w < 3; ++w)
+      if (ssn_forward(e, nullptr, batch, batch, nullptr, nullptr) != SSN_OK)
+        SSN_THROW(SSN_E_RANGE, g_last_error);
+    std::vector<float> ms;
+    for (uint32_t i = 0; i < iters; ++i) {
+      CUDA_TRY(cudaEventRecord(a, e->stream));
+      if (ssn_forward(e, nullptr, batch, batch, nullptr, nullptr) != SSN_OK)
+        SSN_THROW(SSN_E_RANGE, g_last_error);
+      CUDA_TRY(cudaEventRecord(b, e->stream));
+      CUDA_TRY(cudaEventSynchronize(b));
+      float t = 0;
+      CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+      ms.push_back(t);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(ms.begin(), ms.end());
+    *median_us = ms[ms.size() / 2] * 1000.0;
+  });
+}
+
+int ssn_query(ssn_engine* e, ssn_stats* out) {
+  return guarded([&] {
+    if (!e || !out) SSN_THROW(SSN_E_INVALID, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->weight_bytes = e->net.blob_bytes;
+    for (const auto& s : e->subs) {
+      if (!s.ok) continue;
+      ++out->registered_subnets;
+      out->norm_table_bytes += s.norm_bytes;
+      out->max_subnet_stat_bytes = std::max(out->max_subnet_stat_bytes, s.stat_bytes);
+    }
+    out->arena_bytes = e->buf_bytes * NBUF + e->raw_img_bytes * e->desc.max_batch;
+    out->active_subnet = e->active;
+    out->graphs_built = static_cast<uint32_t>(e->graphs.size());
+    out->last_forward_kernels = e->last_kernels;
+    out->last_forward_graphs = e->last_graphs;
+    out->last_actuate_us = e->last_actuate_us;
+    out->last_forward_host_us = e->last_forward_host_us;
+  });
+}
+
+int ssn_device_logits(ssn_engine* e, const float** out) {
+  return guarded([&] {
+    if (!e || !out) SSN_THROW(SSN_E_INVALID, "null argument");
+    *out = e->d_logits;
+  });
+}
+
+// ---- operator-level entry points -----------------------------------------
+
+static OpDesc* op_desc_scratch(const OpDesc& d, cudaStream_t s) {
+  static OpDesc* dev = nullptr;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!dev) CUDA_TRY(cudaMalloc(&dev, sizeof(OpDesc) * 64));
+  static int slot = 0;
+  OpDesc* p = dev + (slot++ % 64);
+  CUDA_TRY(cudaMemcpyAsync(p, &d, sizeof(OpDesc), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return p;
+}
+
+int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wgt, int cout_max,
+                     int cin_max, int k, int stride, int pad, int cout, const float* scale,
+                     const float* shift, const void* res, int act, int out_f32, void* y,
+                     void* stream) {
+  return guarded([&] {
+    if (!x || !wgt || !y) SSN_THROW(SSN_E_INVALID, "null tensor");
+    if (cin % 8 || cin_max % 8 || cout % 8 || cin > cin_max || cout > cout_max || cin <= 0 ||
+        cout <= 0)
+      SSN_THROW(SSN_E_INVALID, "channel counts must be positive multiples of 8 within max shape");
+    if (k < 1 || stride < 1 || pad < 0) SSN_THROW(SSN_E_INVALID, "bad geometry");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(init_conv_tc());
+    OpDesc d{cin, cout, k, pad, scale, shift};
+    ConvParams p{};
+    p.x = x;
+    p.y = y;
+    p.res = res;
+    p.w = wgt;
+    p.row = nullptr;
+    p.fixed = op_desc_scratch(d, s);
+    p.n = n;
+    p.h = h;
+    p.w_ = w;
+    p.ho = (h + 2 * pad - k) / stride + 1;
+    p.wo = (w + 2 * pad - k) / stride + 1;
+    p.stride = stride;
+    p.M = n * p.ho * p.wo;
+    p.k_max = k;
+    p.cin_max = cin_max;
+    p.cout_max = cout_max;
+    p.act = act;
+    p.res_post = 0;
+    p.out_f32 = out_f32;
+    p.bn = choose_bn(cout_max, p.M);
+    CUtensorMap map{};
+    if (make_weight_map(&map, wgt, cin_max, k * k, cout_max, p.bn) != 0)
+      SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
+    CUDA_TRY(launch_conv_tc(p, map, s));
+  });
+}
+
+int ssn_op_conv_f32(const float* x, int n, int h, int w, int cin, const float* wgt, int cout_max,
+                    int cin_max, int k_max, int k, int stride, int pad, int cout, int depthwise,
+                    const float* scale, const float* shift, const float* res, int act, float* y,
+                    void* stream) {
+  return guarded([&] {
+    if (!x || !wgt || !y) SSN_THROW(SSN_E_INVALID, "null tensor");
+    if (cin > cin_max || cout > cout_max || k > k_max || (depthwise && cin != cout))
+      SSN_THROW(SSN_E_INVALID, "active slice exceeds the max shape");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    OpDesc d{cin, cout, k, pad, scale, shift};
+    ConvParams p{};
+    p.x = x;
+    p.y = y;
+    p.res = res;
+    p.w = wgt;
+    p.fixed = op_desc_scratch(d, s);
+    p.n = n;
+    p.h = h;
+    p.w_ = w;
+    p.ho = (h + 2 * pad - k) / stride + 1;
+    p.wo = (w + 2 * pad - k) / stride + 1;
+    p.stride = stride;
+    p.M = n * p.ho * p.wo;
+    p.k_max = k_max;
+    p.cin_max = depthwise ? 1 : cin_max;
+    p.cout_max = cout_max;
+    p.act = act;
+    p.depthwise = depthwise;
+    CUDA_TRY(launch_conv_f32(p, s));
+  });
+}
+
+}  // extern "C"

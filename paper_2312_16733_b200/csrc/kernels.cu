@@ -1,0 +1,259 @@
+// kernels.cu — bandwidth-bound SubNetAct kernels (CUDA cores, sm_100a):
+// input staging, pooling (max / avg-ceil / global), and the float32 SIMT
+// WeightSlice conv used for the config-1 fp32 parity precision.
+//
+// All kernels are subnet-agnostic at launch: active channel counts come from
+// the actuated subnet's OpDesc (device memory), so the same graph-captured
+// launch serves every subnet.  bf16 paths move 8 channels (16 B) per thread
+// access; active widths are multiples of 8 (OFA make_divisible(., 8)).
+#include "../../include/ssn.h"
+#include "device.cuh"
+
+namespace ssn {
+
+// ---------------------------------------------------------------------------
+// input staging: host-format images -> NHWC (bf16 padded to 8 ch, or fp32 3 ch)
+
+__global__ void input_kernel(InputParams p) {
+  const long npix = static_cast<long>(p.n) * p.h * p.w;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < npix;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long hw = static_cast<long>(p.h) * p.w;
+    const long img = i / hw, pix = i - img * hw;
+    float v[3];
+    if (p.format == SSN_INPUT_F32_NCHW) {
+      const float* r = static_cast<const float*>(p.raw) + img * 3 * hw + pix;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = __ldg(r + c * hw);
+    } else {
+      const uint8_t* r = static_cast<const uint8_t*>(p.raw) + i * 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = (static_cast<float>(r[c]) - 128.f) * (1.f / 64.f);
+    }
+    if (p.out_bf16) {
+      uint4 pk;
+      pk.x = pack_bf16x2(v[0], v[1]);
+      pk.y = pack_bf16x2(v[2], 0.f);
+      pk.z = 0u;
+      pk.w = 0u;
+      reinterpret_cast<uint4*>(p.y)[i] = pk;  // 8 channels, 3 real
+    } else {
+      float* y = static_cast<float*>(p.y) + i * 3;
+      y[0] = v[0];
+      y[1] = v[1];
+      y[2] = v[2];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pooling, bf16 NHWC, 8 channels per thread
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 t = __bfloat1622float2(h[q]);
+    f[2 * q] = t.x;
+    f[2 * q + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
+  uint4 u;
+  u.x = pack_bf16x2(f[0], f[1]);
+  u.y = pack_bf16x2(f[2], f[3]);
+  u.z = pack_bf16x2(f[4], f[5]);
+  u.w = pack_bf16x2(f[6], f[7]);
+  return u;
+}
+
+__global__ void pool_bf16_kernel(PoolParams p) {
+  const OpDesc d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin, G = C >> 3;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
+  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y);
+  if (p.kind == 4) {  // global average pool -> [n][C]
+    const long total = static_cast<long>(p.n) * G;
+    const int hw = p.h * p.w;
+    const float inv = 1.f / static_cast<float>(hw);
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+      const long img = i / G;
+      const int g = static_cast<int>(i - img * G);
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const __nv_bfloat16* src = x + img * hw * C + g * 8;
+      for (int q = 0; q < hw; ++q) {
+        float f[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(src + static_cast<long>(q) * C), f);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] += f[t];
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] *= inv;
+      *reinterpret_cast<uint4*>(y + img * C + g * 8) = f32_to_bf16x8(acc);
+    }
+    return;
+  }
+  const long total = static_cast<long>(p.n) * p.ho * p.wo * G;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long opix = i / G;
+    const int g = static_cast<int>(i - opix * G);
+    const long img = opix / (static_cast<long>(p.ho) * p.wo);
+    const int rem = static_cast<int>(opix - img * p.ho * p.wo);
+    const int oh = rem / p.wo, ow = rem - (rem / p.wo) * p.wo;
+    float acc[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t] = p.kind == 2 ? -INFINITY : 0.f;
+    int cnt = 0;
+    for (int r = 0; r < p.k; ++r) {
+      const int ih = oh * p.stride - p.pad + r;
+      if (ih < 0 || ih >= p.h) continue;
+      for (int s = 0; s < p.k; ++s) {
+        const int iw = ow * p.stride - p.pad + s;
+        if (iw < 0 || iw >= p.w) continue;
+        float f[8];
+        bf16x8_to_f32(
+            *reinterpret_cast<const uint4*>(x + ((img * p.h + ih) * p.w + iw) * C + g * 8), f);
+        ++cnt;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = p.kind == 2 ? fmaxf(acc[t], f[t]) : acc[t] + f[t];
+      }
+    }
+    if (p.kind == 3) {
+      const float inv = 1.f / static_cast<float>(cnt);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] *= inv;
+    }
+    *reinterpret_cast<uint4*>(y + opix * C + g * 8) = f32_to_bf16x8(acc);
+  }
+}
+
+__global__ void pool_f32_kernel(PoolParams p) {
+  const OpDesc d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin;
+  const float* x = static_cast<const float*>(p.x);
+  float* y = static_cast<float*>(p.y);
+  if (p.kind == 4) {
+    const long total = static_cast<long>(p.n) * C;
+    const int hw = p.h * p.w;
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+      const long img = i / C;
+      const int c = static_cast<int>(i - img * C);
+      float acc = 0.f;
+      for (int q = 0; q < hw; ++q) acc += x[(img * hw + q) * C + c];
+      y[img * C + c] = acc / static_cast<float>(hw);
+    }
+    return;
+  }
+  const long total = static_cast<long>(p.n) * p.ho * p.wo * C;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long opix = i / C;
+    const int c = static_cast<int>(i - opix * C);
+    const long img = opix / (static_cast<long>(p.ho) * p.wo);
+    const int rem = static_cast<int>(opix - img * p.ho * p.wo);
+    const int oh = rem / p.wo, ow = rem % p.wo;
+    float acc = p.kind == 2 ? -INFINITY : 0.f;
+    int cnt = 0;
+    for (int r = 0; r < p.k; ++r) {
+      const int ih = oh * p.stride - p.pad + r;
+      if (ih < 0 || ih >= p.h) continue;
+      for (int s = 0; s < p.k; ++s) {
+        const int iw = ow * p.stride - p.pad + s;
+        if (iw < 0 || iw >= p.w) continue;
+        const float v = x[((img * p.h + ih) * p.w + iw) * C + c];
+        acc = p.kind == 2 ? fmaxf(acc, v) : acc + v;
+        ++cnt;
+      }
+    }
+    y[opix * C + c] = p.kind == 3 ? acc / static_cast<float>(cnt) : acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// float32 WeightSlice conv / depthwise / linear (SIMT), config-1 precision.
+// weights: dense KRSC [cout_max][k_max][k_max][cin_max]; depthwise
+// [c_max][k_max][k_max]; centre crop to the active k.
+
+__global__ void conv_f32_kernel(ConvParams p) {
+  const OpDesc d = load_desc(p.row, p.fixed, p.op);
+  const long total = static_cast<long>(p.M) * d.cout;
+  const float* x = static_cast<const float*>(p.x);
+  const float* w = static_cast<const float*>(p.w);
+  const int off = (p.k_max - d.k) / 2;
+  const int hwo = p.ho * p.wo;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long m = i / d.cout;
+    const int co = static_cast<int>(i - m * d.cout);
+    const int img = static_cast<int>(m / hwo);
+    const int rem = static_cast<int>(m - static_cast<long>(img) * hwo);
+    const int oh = rem / p.wo, ow = rem % p.wo;
+    float acc = 0.f;
+    for (int r = 0; r < d.k; ++r) {
+      const int ih = oh * p.stride - d.pad + r;
+      if (ih < 0 || ih >= p.h) continue;
+      for (int s = 0; s < d.k; ++s) {
+        const int iw = ow * p.stride - d.pad + s;
+        if (iw < 0 || iw >= p.w_) continue;
+        const float* xp = x + (static_cast<long>(img * p.h + ih) * p.w_ + iw) * d.cin;
+        const int tap = (r + off) * p.k_max + (s + off);
+        if (p.depthwise) {
+          acc += xp[co] * __ldg(w + static_cast<long>(co) * p.k_max * p.k_max + tap);
+        } else {
+          const float* wp = w + (static_cast<long>(co) * p.k_max * p.k_max + tap) * p.cin_max;
+          for (int ci = 0; ci < d.cin; ++ci) acc += xp[ci] * __ldg(wp + ci);
+        }
+      }
+    }
+    float v = acc * (d.scale ? d.scale[co] : 1.f) + (d.shift ? d.shift[co] : 0.f);
+    const float* res = static_cast<const float*>(p.res);
+    if (res && !p.res_post) v += res[m * d.cout + co];
+    if (p.act == 1) v = fmaxf(v, 0.f);
+    if (res && p.res_post) v += res[m * d.cout + co];
+    static_cast<float*>(p.y)[m * d.cout + co] = v;
+  }
+}
+
+__global__ void set_row_kernel(const OpDesc** slot, const OpDesc* row) { *slot = row; }
+
+// ---------------------------------------------------------------------------
+// launchers
+
+static inline int grid_for(long work, int block) {
+  long g = (work + block - 1) / block;
+  const long cap = 148L * 16;
+  if (g > cap) g = cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_input(const InputParams& p, cudaStream_t s) {
+  input_kernel<<<grid_for(static_cast<long>(p.n) * p.h * p.w, 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// `max_c` bounds the grid for the largest subnet; surplus threads exit.
+cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s) {
+  const long per = bf16 ? max_c / 8 : max_c;
+  const long work = p.kind == 4 ? static_cast<long>(p.n) * per
+                                : static_cast<long>(p.n) * p.ho * p.wo * per;
+  if (bf16)
+    pool_bf16_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
+  else
+    pool_f32_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s) {
+  conv_f32_kernel<<<grid_for(static_cast<long>(p.M) * p.cout_max, 128), 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s) {
+  set_row_kernel<<<1, 1, 0, s>>>(slot, row);
+  return cudaGetLastError();
+}
+
+}  // namespace ssn

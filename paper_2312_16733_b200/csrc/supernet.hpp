@@ -1,0 +1,587 @@
+// supernet.hpp — supernet layer plans for the SubNetAct engine (host C++).
+//
+// A supernet is a fixed list of max-shape ops grouped into blocks and
+// segments.  Resolving a subnet control tuple (D, E, W[, K]) — the engine's
+// view of servesim::SubnetConfig (reference profile.hpp:28-54) — fills in each
+// op's ACTIVE widths (WeightSlice), marks skipped blocks
+// (LayerSelect) and assigns each active norm layer its slot
+// in the subnet's SubnetNorm statistics row.
+//
+// The op order and tensor/norm ordinals are the canonical ones of DESIGN.md
+// §3-§5 (the oracle restates them independently in oracle/ssn_oracle.c).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ssn.h"
+#include "../../include/ssn_rng.h"
+
+namespace ssn {
+
+enum OpKind : int {
+  OP_INPUT = 0,    // raw host-format images -> NHWC activations
+  OP_CONV = 1,     // WeightSlice conv (+SubnetNorm +act +residual)
+  OP_MAXPOOL = 2,  // 3x3 s2 p1
+  OP_AVGPOOL = 3,  // k = s, ceil_mode
+  OP_GAP = 4,      // global average pool -> [N][C]
+  OP_LINEAR = 5,   // classifier (fp32 logits)
+};
+
+// Logical buffer slots inside a block; mapped to arena buffers per graph.
+enum Slot : int {
+  S_NONE = -1,
+  S_IN = 0,
+  S_OUT = 1,
+  S_T1 = 2,
+  S_T2 = 3,
+  S_T3 = 4,
+  S_RAW = 5,     // input staging (raw host format)
+  S_LOGITS = 6,  // fp32 logits
+};
+
+enum Act : int { ACT_NONE = 0, ACT_RELU = 1 };
+
+struct TensorSpec {
+  int cout = 0, cin = 0, k = 1;  // max shape (depthwise: cin == 1)
+  int cin_store = 0;             // stored inner dim (>= cin, multiple of 8 for bf16)
+  bool depthwise = false, linear = false;
+  uint32_t fan_in = 1;
+  uint64_t w_off = 0, w_bytes = 0;  // blob offsets
+  uint64_t b_off = 0;               // bias (linear), fp32
+};
+
+struct NormSpec {
+  int c = 0;
+  bool res = false;  // last norm of a residual branch (gamma ~ U(0, SSN_RES_GAMMA))
+  uint64_t gamma_off = 0, beta_off = 0;  // fp32 in the blob
+};
+
+struct OpSpec {
+  int kind = OP_CONV;
+  int in = S_IN, out = S_OUT, res = S_NONE;
+  bool res_post = false;  // residual added after the activation
+  int tensor = -1, norm = -1;
+  int act = ACT_NONE;
+  int stride = 1, k_max = 1, pool_k = 0;
+  int hin = 0, win = 0, hout = 0, wout = 0;
+  int cin_max = 0, cout_max = 0;  // cin_max = stored inner dim
+  bool depthwise = false;
+  // ---- resolved for one subnet ----
+  bool active = true;
+  int cin = 0, cout = 0, k = 1;
+  int64_t stat_off = -1;   // offset into the subnet's statistics row
+  int norm_slot = -1;      // index among the subnet's active norm layers
+};
+
+struct BlockSpec {
+  int first = 0, count = 0;
+  int flag = -1;  // LayerSelect flag index (-1 = always runs)
+  int segment = 0;
+};
+
+struct SegmentSpec {
+  std::vector<int> blocks;
+  std::vector<int> flags;  // distinct flags of the segment (variant bits)
+};
+
+struct Net {
+  ssn_supernet_desc desc{};
+  std::vector<TensorSpec> tensors;
+  std::vector<NormSpec> norms;
+  std::vector<OpSpec> ops;
+  std::vector<BlockSpec> blocks;
+  std::vector<SegmentSpec> segments;
+  uint64_t blob_bytes = 0;
+  int n_flags = 0;
+  uint64_t stat_count = 0;  // for the resolved subnet
+  int elem_bytes = 2;
+};
+
+// Control tuple in engine form.
+struct SubnetCfg {
+  std::vector<uint8_t> depth;
+  std::vector<double> expand;
+  std::vector<double> width;
+  std::vector<uint32_t> kernel;
+  static SubnetCfg from_c(const ssn_subnet_cfg* c) {
+    SubnetCfg s;
+    if (!c) return s;
+    if (c->depth_flags) s.depth.assign(c->depth_flags, c->depth_flags + c->n_depth);
+    if (c->expand_ratios) s.expand.assign(c->expand_ratios, c->expand_ratios + c->n_expand);
+    if (c->width_multipliers)
+      s.width.assign(c->width_multipliers, c->width_multipliers + c->n_width);
+    if (c->kernel_sizes) s.kernel.assign(c->kernel_sizes, c->kernel_sizes + c->n_kernel);
+    return s;
+  }
+};
+
+inline int md8(double v) { return ssn_make_divisible(v, 8); }
+inline int rnd(double v) { return ssn_round_half_even(v); }
+
+// ---------------------------------------------------------------------------
+// builder helpers
+
+class Builder {
+ public:
+  explicit Builder(Net& n) : net(n) {}
+
+  int tensor(int cout, int cin, int k, bool dw, bool linear, int cin_store = 0) {
+    TensorSpec t;
+    t.cout = cout;
+    t.cin = dw ? 1 : cin;
+    t.k = k;
+    t.depthwise = dw;
+    t.linear = linear;
+    t.cin_store = dw ? 1 : (cin_store ? cin_store : cin);
+    t.fan_in = static_cast<uint32_t>(t.cin * k * k);
+    net.tensors.push_back(t);
+    return static_cast<int>(net.tensors.size()) - 1;
+  }
+  int norm(int c, bool res = false) {
+    NormSpec n;
+    n.c = c;
+    n.res = res;
+    net.norms.push_back(n);
+    return static_cast<int>(net.norms.size()) - 1;
+  }
+  void begin_block(int flag) {
+    BlockSpec b;
+    b.first = static_cast<int>(net.ops.size());
+    b.flag = flag;
+    b.segment = cur_segment;
+    net.blocks.push_back(b);
+  }
+  void end_block() {
+    auto& b = net.blocks.back();
+    b.count = static_cast<int>(net.ops.size()) - b.first;
+    net.segments[cur_segment].blocks.push_back(static_cast<int>(net.blocks.size()) - 1);
+    if (b.flag >= 0) net.segments[cur_segment].flags.push_back(b.flag);
+  }
+  void begin_segment() {
+    net.segments.emplace_back();
+    cur_segment = static_cast<int>(net.segments.size()) - 1;
+  }
+  OpSpec& op(int kind) {
+    net.ops.emplace_back();
+    net.ops.back().kind = kind;
+    return net.ops.back();
+  }
+
+  Net& net;
+  int cur_segment = -1;
+};
+
+inline void finalize_layout(Net& net) {
+  // Blob: weight tensors (256-B aligned), then fp32 biases, gammas, betas.
+  const int eb = net.elem_bytes;
+  uint64_t off = 0;
+  auto align = [](uint64_t v) { return (v + 255) & ~uint64_t(255); };
+  for (auto& t : net.tensors) {
+    off = align(off);
+    t.w_off = off;
+    t.w_bytes = uint64_t(t.cout) * t.k * t.k * t.cin_store * eb;
+    off += t.w_bytes;
+  }
+  for (auto& t : net.tensors) {
+    if (!t.linear) continue;
+    off = align(off);
+    t.b_off = off;
+    off += uint64_t(t.cout) * 4;
+  }
+  for (auto& n : net.norms) {
+    off = align(off);
+    n.gamma_off = off;
+    off += uint64_t(n.c) * 4;
+    off = align(off);
+    n.beta_off = off;
+    off += uint64_t(n.c) * 4;
+  }
+  net.blob_bytes = align(off);
+  net.n_flags = 0;
+  for (auto& b : net.blocks) net.n_flags = std::max(net.n_flags, b.flag + 1);
+}
+
+// Assign statistics slots to active norm layers in execution order.
+inline void assign_stats(Net& net) {
+  uint64_t cursor = 0;
+  int slot = 0;
+  for (auto& o : net.ops) {
+    if (!o.active || o.norm < 0) continue;
+    o.stat_off = static_cast<int64_t>(cursor);
+    o.norm_slot = slot++;
+    cursor += static_cast<uint64_t>(o.cout);
+  }
+  net.stat_count = cursor;
+}
+
+inline void mark_blocks(Net& net, const std::vector<uint8_t>& depth) {
+  for (auto& b : net.blocks) {
+    const bool on = b.flag < 0 || depth[b.flag];
+    for (int i = 0; i < b.count; ++i) net.ops[b.first + i].active = on;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Config 1 — TinyCNN. D = 5, E = 3, W = 4.
+
+inline Net build_tinycnn(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
+  static const int BASE[4] = {32, 32, 64, 128};
+  static const double MAX_E = 6.0;
+  struct B { int stage, stride, flag; bool res; };
+  static const B BLK[8] = {{0, 1, -1, false}, {0, 1, 0, true}, {0, 1, 1, true},
+                           {1, 2, -1, false}, {1, 1, 2, true}, {1, 1, 3, true},
+                           {2, 2, -1, false}, {2, 1, 4, true}};
+  SubnetCfg mx;
+  mx.depth.assign(5, 1);
+  mx.expand.assign(3, MAX_E);
+  mx.width.assign(4, 1.0);
+  const SubnetCfg& s = cfg ? *cfg : mx;
+  if (s.depth.size() != 5 || s.expand.size() != 3 || s.width.size() != 4)
+    throw std::invalid_argument(
+        "tinycnn subnet needs 5 depth flags, 3 expand ratios, 4 width multipliers");
+  for (double e : s.expand)
+    if (!(e > 0.0) || e > MAX_E) throw std::invalid_argument("expand ratio must be in (0, 6]");
+  for (double w : s.width)
+    if (!(w > 0.0) || w > 1.0) throw std::invalid_argument("width multiplier must be in (0,1]");
+
+  Net net;
+  net.desc = d;
+  net.elem_bytes = d.dtype == SSN_DTYPE_BF16 ? 2 : 4;
+  const bool bf16 = d.dtype == SSN_DTYPE_BF16;
+  Builder b(net);
+  const int H = static_cast<int>(d.image_size);
+  int C[4];
+  for (int i = 0; i < 4; ++i) C[i] = md8(BASE[i] * s.width[i]);
+
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_INPUT);
+    o.in = S_RAW;
+    o.hin = o.hout = H;
+    o.win = o.wout = H;
+    o.cin_max = 3;
+    o.cout_max = o.cout = bf16 ? 8 : 3;
+    o.cin = 3;
+  }
+  b.end_block();
+  const int t_stem = b.tensor(BASE[0], 3, 3, false, false, bf16 ? 8 : 3);
+  const int n_stem = b.norm(BASE[0]);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);
+    o.tensor = t_stem;
+    o.norm = n_stem;
+    o.act = ACT_RELU;
+    o.k_max = o.k = 3;
+    o.stride = 1;
+    o.hin = o.hout = H;
+    o.win = o.wout = H;
+    o.cin_max = bf16 ? 8 : 3;
+    o.cin = bf16 ? 8 : 3;
+    o.cout_max = BASE[0];
+    o.cout = C[0];
+  }
+  b.end_block();
+
+  int hw = H, cin_max = BASE[0], cin_a = C[0];
+  int stage_seen = -1;
+  for (int bi = 0; bi < 8; ++bi) {
+    const B& blk = BLK[bi];
+    if (blk.stage != stage_seen) {
+      b.begin_segment();
+      stage_seen = blk.stage;
+    }
+    const int cout_max = BASE[1 + blk.stage];
+    const int hid_max = md8(rnd(cin_max * MAX_E));
+    const int t1 = b.tensor(hid_max, cin_max, 1, false, false);
+    const int n1 = b.norm(hid_max);
+    const int t2 = b.tensor(hid_max, hid_max, 3, true, false);
+    const int n2 = b.norm(hid_max);
+    const int t3 = b.tensor(cout_max, hid_max, 1, false, false);
+    const int n3 = b.norm(cout_max, blk.res);
+    const bool on = blk.flag < 0 || s.depth[blk.flag];
+    // active dims of this block (a skipped block forwards its input)
+    const int cout_a = C[1 + blk.stage];
+    const int hid = md8(rnd(cin_a * s.expand[blk.stage]));
+    const int hw_out = (hw + 2 - 3) / blk.stride + 1;
+    b.begin_block(blk.flag);
+    {
+      auto& o = b.op(OP_CONV);
+      o.in = S_IN; o.out = S_T1;
+      o.tensor = t1; o.norm = n1; o.act = ACT_RELU;
+      o.hin = o.hout = hw; o.win = o.wout = hw;
+      o.cin_max = cin_max; o.cout_max = hid_max;
+      o.cin = cin_a; o.cout = hid;
+    }
+    {
+      auto& o = b.op(OP_CONV);
+      o.in = S_T1; o.out = S_T2;
+      o.tensor = t2; o.norm = n2; o.act = ACT_RELU;
+      o.depthwise = true;
+      o.k_max = o.k = 3; o.stride = blk.stride;
+      o.hin = hw; o.win = hw; o.hout = hw_out; o.wout = hw_out;
+      o.cin_max = hid_max; o.cout_max = hid_max;
+      o.cin = hid; o.cout = hid;
+    }
+    {
+      auto& o = b.op(OP_CONV);
+      o.in = S_T2; o.out = S_OUT;
+      o.res = blk.res ? S_IN : S_NONE;
+      o.tensor = t3; o.norm = n3; o.act = ACT_NONE;
+      o.hin = o.hout = hw_out; o.win = o.wout = hw_out;
+      o.cin_max = hid_max; o.cout_max = cout_max;
+      o.cin = hid; o.cout = cout_a;
+    }
+    b.end_block();
+    if (blk.res && on && cin_a != cout_a)
+      throw std::invalid_argument("residual block shape mismatch");
+    if (on) cin_a = cout_a;
+    cin_max = cout_max;
+    hw = hw_out;
+  }
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_GAP);
+    o.hin = o.win = hw;
+    o.hout = o.wout = 1;
+    o.cin_max = o.cout_max = BASE[3];
+    o.cin = o.cout = cin_a;
+  }
+  b.end_block();
+  const int tl = b.tensor(static_cast<int>(d.num_classes), BASE[3], 1, false, true);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_LINEAR);
+    o.out = S_LOGITS;
+    o.tensor = tl;
+    o.hin = o.win = o.hout = o.wout = 1;
+    o.cin_max = BASE[3];
+    o.cout_max = static_cast<int>(d.num_classes);
+    o.cin = cin_a;
+    o.cout = static_cast<int>(d.num_classes);
+  }
+  b.end_block();
+  finalize_layout(net);
+  mark_blocks(net, s.depth);
+  assign_stats(net);
+  return net;
+}
+
+// ---------------------------------------------------------------------------
+// Config 2 — OFA-ResNet50. D = 9 per-block flags, E = 18,
+// W = 6.  Layout follows OFA's OFAResNets / DynamicResNetBottleneckBlock
+// [external]: stem (conv3x3 s2, residual conv3x3, conv3x3), maxpool, 4 stages
+// of bottlenecks (base depth 2/2/4/2, +2 optional), avgpool_conv downsample.
+
+inline Net build_ofa_resnet50(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
+  static const int STAGE_W[4] = {256, 512, 1024, 2048};
+  static const int BASE_DEPTH[4] = {2, 2, 4, 2};
+  static const int NBLK[4] = {4, 4, 6, 4};
+  static const double MAX_E = 0.35;
+  SubnetCfg mx;
+  mx.depth.assign(9, 1);
+  mx.expand.assign(18, MAX_E);
+  mx.width.assign(6, 1.0);
+  const SubnetCfg& s = cfg ? *cfg : mx;
+  if (s.depth.size() != 9 || s.expand.size() != 18 || s.width.size() != 6)
+    throw std::invalid_argument(
+        "ofa_resnet50 subnet needs 9 depth flags, 18 expand ratios, 6 width multipliers");
+  for (double w : s.width)
+    if (!(w > 0.0) || w > 1.0) throw std::invalid_argument("width multiplier must be in (0,1]");
+  for (double e : s.expand)
+    if (!(e > 0.0)) throw std::invalid_argument("expand ratio must be > 0");
+
+  Net net;
+  net.desc = d;
+  const bool bf16 = d.dtype == SSN_DTYPE_BF16;
+  net.elem_bytes = bf16 ? 2 : 4;
+  Builder b(net);
+  const int H = static_cast<int>(d.image_size);
+  const int stem_mid_a = md8(md8(64 * s.width[0]) / 2);
+  const int stem_out_a = md8(64 * s.width[1]);
+  const int cin0 = bf16 ? 8 : 3;
+
+  // ---- segment 0: input, stem, maxpool
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_INPUT);
+    o.in = S_RAW;
+    o.hin = o.hout = H; o.win = o.wout = H;
+    o.cin_max = 3; o.cin = 3;
+    o.cout_max = o.cout = cin0;
+  }
+  b.end_block();
+  const int H2 = (H + 2 - 3) / 2 + 1;
+  const int t0 = b.tensor(32, 3, 3, false, false, cin0);
+  const int n0 = b.norm(32);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);
+    o.tensor = t0; o.norm = n0; o.act = ACT_RELU;
+    o.k_max = o.k = 3; o.stride = 2;
+    o.hin = H; o.win = H; o.hout = H2; o.wout = H2;
+    o.cin_max = cin0; o.cin = cin0;
+    o.cout_max = 32; o.cout = stem_mid_a;
+  }
+  b.end_block();
+  const int t1 = b.tensor(32, 32, 3, false, false);
+  const int n1 = b.norm(32, true);
+  b.begin_block(0);
+  {
+    auto& o = b.op(OP_CONV);
+    o.tensor = t1; o.norm = n1; o.act = ACT_RELU;
+    o.res = S_IN; o.res_post = true;
+    o.k_max = o.k = 3; o.stride = 1;
+    o.hin = o.hout = H2; o.win = o.wout = H2;
+    o.cin_max = 32; o.cin = stem_mid_a;
+    o.cout_max = 32; o.cout = stem_mid_a;
+  }
+  b.end_block();
+  const int t2 = b.tensor(64, 32, 3, false, false);
+  const int n2 = b.norm(64);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);
+    o.tensor = t2; o.norm = n2; o.act = ACT_RELU;
+    o.k_max = o.k = 3; o.stride = 1;
+    o.hin = o.hout = H2; o.win = o.wout = H2;
+    o.cin_max = 32; o.cin = stem_mid_a;
+    o.cout_max = 64; o.cout = stem_out_a;
+  }
+  b.end_block();
+  const int H4 = (H2 + 2 - 3) / 2 + 1;
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_MAXPOOL);
+    o.k_max = o.k = 3; o.stride = 2;
+    o.hin = o.win = H2; o.hout = o.wout = H4;
+    o.cin_max = o.cout_max = 64;
+    o.cin = o.cout = stem_out_a;
+  }
+  b.end_block();
+
+  // ---- segments 1..4: bottleneck stages
+  int hw = H4, cin_max = 64, cin_a = stem_out_a, blk_idx = 0;
+  for (int st = 0; st < 4; ++st) {
+    b.begin_segment();
+    const int out_max = STAGE_W[st];
+    const int mid_max = md8(rnd(out_max * MAX_E));
+    const int out_a = md8(out_max * s.width[2 + st]);
+    const int stride = st == 0 ? 1 : 2;
+    for (int bi = 0; bi < NBLK[st]; ++bi, ++blk_idx) {
+      const int flag = bi >= BASE_DEPTH[st] ? 1 + 2 * st + (bi - BASE_DEPTH[st]) : -1;
+      const int mid_a = md8(rnd(out_a * s.expand[blk_idx]));
+      if (mid_a > mid_max)
+        throw std::invalid_argument("expand ratio exceeds the supernet's max middle width");
+      const bool first = bi == 0;
+      const int st_ = first ? stride : 1;
+      const int hw_out = (hw + 2 - 3) / st_ + 1;
+      b.begin_block(flag);
+      if (first) {
+        const int td = b.tensor(out_max, cin_max, 1, false, false);
+        const int nd = b.norm(out_max);
+        int ds_in = S_IN;
+        if (stride > 1) {
+          auto& p = b.op(OP_AVGPOOL);
+          p.in = S_IN; p.out = S_T1;
+          p.pool_k = p.stride = stride;
+          p.k_max = p.k = stride;
+          p.hin = p.win = hw;
+          p.hout = p.wout = (hw + stride - 1) / stride;
+          p.cin_max = p.cout_max = cin_max;
+          p.cin = p.cout = cin_a;
+          ds_in = S_T1;
+        }
+        auto& o = b.op(OP_CONV);
+        o.in = ds_in; o.out = S_T3;
+        o.tensor = td; o.norm = nd; o.act = ACT_NONE;
+        o.hin = o.win = o.hout = o.wout = (hw + stride - 1) / stride;
+        o.cin_max = cin_max; o.cin = cin_a;
+        o.cout_max = out_max; o.cout = out_a;
+      }
+      const int ta = b.tensor(mid_max, cin_max, 1, false, false);
+      const int na = b.norm(mid_max);
+      const int tb = b.tensor(mid_max, mid_max, 3, false, false);
+      const int nb = b.norm(mid_max);
+      const int tc = b.tensor(out_max, mid_max, 1, false, false);
+      const int nc = b.norm(out_max, true);
+      {
+        auto& o = b.op(OP_CONV);
+        o.in = S_IN; o.out = S_T1;
+        o.tensor = ta; o.norm = na; o.act = ACT_RELU;
+        o.hin = o.hout = hw; o.win = o.wout = hw;
+        o.cin_max = cin_max; o.cin = cin_a;
+        o.cout_max = mid_max; o.cout = mid_a;
+      }
+      {
+        auto& o = b.op(OP_CONV);
+        o.in = S_T1; o.out = S_T2;
+        o.tensor = tb; o.norm = nb; o.act = ACT_RELU;
+        o.k_max = o.k = 3; o.stride = st_;
+        o.hin = hw; o.win = hw; o.hout = hw_out; o.wout = hw_out;
+        o.cin_max = mid_max; o.cin = mid_a;
+        o.cout_max = mid_max; o.cout = mid_a;
+      }
+      {
+        auto& o = b.op(OP_CONV);
+        o.in = S_T2; o.out = S_OUT;
+        o.res = first ? S_T3 : S_IN;
+        o.tensor = tc; o.norm = nc; o.act = ACT_RELU;
+        o.hin = o.hout = hw_out; o.win = o.wout = hw_out;
+        o.cin_max = mid_max; o.cin = mid_a;
+        o.cout_max = out_max; o.cout = out_a;
+      }
+      b.end_block();
+      const bool on = flag < 0 || s.depth[flag];
+      if (on) cin_a = out_a;
+      cin_max = out_max;
+      hw = hw_out;
+    }
+  }
+
+  // ---- segment 5: global pool + classifier
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_GAP);
+    o.hin = o.win = hw;
+    o.hout = o.wout = 1;
+    o.cin_max = o.cout_max = 2048;
+    o.cin = o.cout = cin_a;
+  }
+  b.end_block();
+  const int tl = b.tensor(static_cast<int>(d.num_classes), 2048, 1, false, true);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_LINEAR);
+    o.out = S_LOGITS;
+    o.tensor = tl;
+    o.hin = o.win = o.hout = o.wout = 1;
+    o.cin_max = 2048;
+    o.cout_max = static_cast<int>(d.num_classes);
+    o.cin = cin_a;
+    o.cout = static_cast<int>(d.num_classes);
+  }
+  b.end_block();
+  finalize_layout(net);
+  mark_blocks(net, s.depth);
+  assign_stats(net);
+  return net;
+}
+
+inline Net build_net(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
+  switch (d.family) {
+    case SSN_FAMILY_TINYCNN: return build_tinycnn(d, cfg);
+    case SSN_FAMILY_OFA_RESNET50: return build_ofa_resnet50(d, cfg);
+    default: throw std::invalid_argument("unsupported supernet family");
+  }
+}
+
+}  // namespace ssn

@@ -1,0 +1,190 @@
+"""End-to-end SubNetAct engine parity on the GPU, through the C-ABI.
+
+Every subnet's logits are compared with the CPU oracle on the same seeded
+images, weights (ssn_rng.h) and SubnetNorm statistics:
+  * config 1 (TinyCNN, fp32):  rel L2 error <= 1e-4, argmax identical;
+  * config 2 (OFA-ResNet50, bf16 storage / fp32 accumulate):
+      vs the oracle with bf16 activation storage emulated: rel <= 2e-2
+      vs the pure-fp32 oracle:                           rel <= 2e-2
+    argmax identical wherever the oracle's top-2 margin exceeds the error.
+SubnetNorm statistics are calibrated by the oracle (batch statistics over a
+separate calibration batch) and handed to
+ssn_register_subnet, or left to the engine's deterministic defaults.
+"""
+import numpy as np
+import pytest
+
+import paper_2312_16733_b200 as ssn
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SEED = 0
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-12))
+
+
+def argmax_agree(got, ref, tol):
+    """Argmax must agree on rows whose reference top-2 margin exceeds tol."""
+    top2 = np.sort(ref, axis=1)[:, -2:]
+    margin = top2[:, 1] - top2[:, 0]
+    clear = margin > tol
+    assert (got.argmax(1)[clear] == ref.argmax(1)[clear]).all()
+    return int((~clear).sum())
+
+
+# ---------------------------------------------------------------- config 1
+TINY_SUBNETS = [c for _, _, c in ssn.default_catalog_configs()] + [
+    ssn.tinycnn_config([False, True, False, True, False], [3.0, 4.0, 6.0], [0.6] * 4),
+    ssn.tinycnn_config([False] * 5, [2.0, 3.0, 4.0], [0.4, 0.7, 0.5, 1.0]),
+    ssn.tinycnn_config([True, False, True, False, True], [6.0, 6.0, 6.0], [1.0, 0.4, 1.0, 0.4]),
+]
+
+
+@pytest.fixture(scope="module")
+def tiny(gpu):
+    desc = ssn.make_desc(ssn.FAMILY_TINYCNN, ssn.DTYPE_F32, image_size=32, num_classes=10,
+                         max_batch=8, seed=SEED)
+    eng = ssn.Engine(desc)
+    on = O.OracleNet(ssn.FAMILY_TINYCNN, seed=SEED, classes=10, bf16_weights=False)
+    cal = O.images(SEED, 100, 8, 32)
+    stats = []
+    for i, cfg in enumerate(TINY_SUBNETS):
+        m, v = on.calibrate(cfg, cal)
+        eng.register_subnet(i, cfg, m, v)
+        stats.append((m, v))
+    eng.prepare([1, 2, 4, 8])
+    yield eng, on, stats
+    eng.close()
+
+
+@pytest.mark.parametrize("i", range(len(TINY_SUBNETS)))
+def test_tinycnn_fp32_parity(tiny, i):
+    eng, on, stats = tiny
+    x = O.images(SEED, 1, 8, 32)
+    eng.actuate(i)
+    got = eng.infer(x, 8, 8)
+    ref = on.forward(TINY_SUBNETS[i], x, mean=stats[i][0], var=stats[i][1])
+    assert rel(got, ref) <= 1e-4, rel(got, ref)
+    assert (got.argmax(1) == ref.argmax(1)).all()
+
+
+def test_tinycnn_padded_batch_and_switching(tiny):
+    eng, on, stats = tiny
+    x = O.images(SEED, 2, 8, 32)
+    eng.actuate(2)
+    full = eng.infer(x, 8, 8)
+    eng.actuate(5)
+    other = eng.infer(x, 8, 8)
+    eng.actuate(2)
+    part = eng.infer(x[:5], 5, 8)  # ClampedDispatch: 5 real images padded to 8
+    np.testing.assert_array_equal(part, full[:5])
+    again = eng.infer(x, 8, 8)
+    np.testing.assert_array_equal(again, full)
+    assert rel(other, full) > 1e-3  # different subnet, different function
+    st = eng.stats()
+    assert st["active_subnet"] == 2 and st["registered_subnets"] == len(TINY_SUBNETS)
+
+
+def test_engine_errors_mirror_reference(tiny):
+    eng, on, stats = tiny
+    with pytest.raises(IndexError):
+        eng.actuate(999)  # unknown subnet: std::out_of_range (profile.hpp:146)
+    x = O.images(SEED, 1, 4, 32)
+    eng.actuate(0)
+    with pytest.raises(IndexError):
+        eng.infer(x, 3, 3)  # batch not profiled / prepared (profile.hpp:78-80)
+    with pytest.raises(ValueError):
+        eng.register_subnet(50, ssn.tinycnn_config([True] * 5, [3.0, 4.0, 6.0], [1.2] * 4))
+    with pytest.raises(ValueError):
+        eng.register_subnet(50, ssn.tinycnn_config([True] * 4, [3.0, 4.0, 6.0], [1.0] * 4))
+
+
+# ---------------------------------------------------------------- config 2
+R50_HW = 64
+
+
+@pytest.fixture(scope="module")
+def r50(gpu):
+    desc = ssn.make_desc(ssn.FAMILY_OFA_RESNET50, ssn.DTYPE_BF16, image_size=R50_HW,
+                         num_classes=1000, max_batch=16, seed=SEED)
+    eng = ssn.Engine(desc)
+    on = O.OracleNet(ssn.FAMILY_OFA_RESNET50, seed=SEED, classes=1000, bf16_weights=True)
+    eng.prepare([1, 4, 8, 16])
+    yield eng, on, desc
+    eng.close()
+
+
+R50_CASES = {
+    "min": ssn.ofa_resnet50_preset("min"),
+    "mid": ssn.ofa_resnet50_preset("mid"),
+    "max": ssn.ofa_resnet50_preset("max"),
+    "mixed": ssn.ofa_resnet50_config([2, 0, 1, 2, 0], [0.2, 0.35, 0.25] * 6, [2, 0, 1, 2, 0, 1]),
+    "skips": ssn.ofa_resnet50_config([0, 2, 0, 1, 2], [0.35] * 18, [0, 2, 1, 0, 2, 2]),
+}
+
+
+@pytest.mark.parametrize("name", list(R50_CASES))
+def test_ofa_resnet50_bf16_parity(r50, name):
+    eng, on, desc = r50
+    cfg = R50_CASES[name]
+    sid = list(R50_CASES).index(name)
+    m, v = on.calibrate(cfg, O.images(SEED, 100, 16, R50_HW))
+    eng.register_subnet(sid, cfg, m, v)
+    x = O.images(SEED, 7, 16, R50_HW)
+    eng.actuate(sid)
+    got = eng.infer(x, 16, 16)
+    emu = on.forward(cfg, x, mean=m, var=v, bf16_storage=True)
+    ref = on.forward(cfg, x, mean=m, var=v)
+    e_emu, e_ref = rel(got, emu), rel(got, ref)
+    print(f"{name}: rel vs bf16-storage oracle {e_emu:.2e}, vs fp32 oracle {e_ref:.2e}")
+    assert e_emu <= 2e-2
+    assert e_ref <= 2e-2
+    argmax_agree(got, ref, tol=4 * e_ref * np.abs(ref).max())
+
+
+def test_ofa_resnet50_default_stats_and_padding(r50):
+    eng, on, desc = r50
+    cfg = R50_CASES["mid"]
+    eng.register_subnet(40, cfg)  # deterministic default SubnetNorm rows
+    x = O.images(SEED, 9, 8, R50_HW)
+    eng.actuate(40)
+    got = eng.infer(x, 8, 8)
+    ref = on.forward(cfg, x, subnet_id=40, bf16_storage=True)
+    assert rel(got, ref) <= 2e-2, rel(got, ref)
+    part = eng.infer(x[:3], 3, 4)
+    np.testing.assert_array_equal(part, eng.infer(x[:3], 3, 4))
+    assert rel(part, got[:3]) < 1e-6  # padding rows never touch real rows
+
+
+def test_ofa_resnet50_u8_input(gpu):
+    desc = ssn.make_desc(ssn.FAMILY_OFA_RESNET50, ssn.DTYPE_BF16, image_size=32,
+                         num_classes=1000, max_batch=4, seed=SEED,
+                         input_format=ssn.INPUT_U8_NHWC)
+    cfg = R50_CASES["min"]
+    on = O.OracleNet(ssn.FAMILY_OFA_RESNET50, seed=SEED, classes=1000)
+    with ssn.Engine(desc) as eng:
+        eng.register_subnet(0, cfg)
+        eng.prepare([4])
+        eng.actuate(0)
+        u8 = np.random.default_rng(0).integers(0, 256, (4, 32, 32, 3), dtype=np.uint8)
+        got = eng.infer(u8, 4, 4)
+        x = ((u8.astype(np.float32) - 128.0) / 64.0).transpose(0, 3, 1, 2)
+        ref = on.forward(cfg, x, subnet_id=0, bf16_storage=True)
+        assert rel(got, ref) <= 2e-2
+
+
+def test_actuation_moves_no_weights(r50):
+    eng, on, desc = r50
+    before = eng.stats()
+    for sid in (0, 1, 2):
+        eng.register_subnet(sid, R50_CASES[list(R50_CASES)[sid]])
+    x = O.images(SEED, 3, 4, R50_HW)
+    for sid in (0, 2, 1, 0):
+        eng.actuate(sid)
+        eng.infer(x, 4, 4)
+    st = eng.stats()
+    assert st["weight_bytes"] == before["weight_bytes"] == ssn.weight_blob_bytes(desc)
+    assert st["last_actuate_us"] < 1000.0

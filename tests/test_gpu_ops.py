@@ -1,0 +1,118 @@
+"""Operator-level parity on the GPU: WeightSlice conv (+ SubnetNorm epilogue,
+residual, activation) through the C-ABI (ssn_op_conv_*), against the CPU
+oracle (oracle/ssn_oracle.c:oracle_conv_op) on the same seeded tensors.
+
+bf16 path: inputs and weights are bf16 values; the oracle computes in fp64
+accumulation on those same values, so the only differences are the GPU's
+fp32 accumulation order and the final bf16 rounding of the output
+(tolerance: 1e-2 relative to the output scale, written per test).
+"""
+import numpy as np
+import pytest
+
+import paper_2312_16733_b200 as ssn
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16)
+
+
+def _run_bf16(gpu, n, h, w, cin, cin_max, cout, cout_max, k, stride, res=False, act=1,
+              out_f32=False, seed=0):
+    import torch
+    rng = np.random.default_rng(seed)
+    pad = k // 2
+    x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+    wmax = (rng.standard_normal((cout_max, cin_max, k, k)) / np.sqrt(cin * k * k)).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32)
+    shift = rng.uniform(-0.2, 0.2, cout).astype(np.float32)
+    xb = _bf16(x)
+    wb = _bf16(wmax)
+    x_r = xb.float().numpy()
+    w_r = wb.float().numpy()
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    r = rng.standard_normal((n, ho, wo, cout)).astype(np.float32) if res else None
+    rb = _bf16(r) if res else None
+    ref = O.conv_op(x_r, w_r, cout_max, cin_max, k, k, stride, pad, cout, scale=scale,
+                    shift=shift, res=None if rb is None else rb.float().numpy(), act=act)
+    # device tensors: x NHWC compact, weights KRSC max shape
+    xd = xb.to(gpu).contiguous()
+    wd = wb.permute(0, 2, 3, 1).contiguous().to(gpu)  # [cout][k][k][cin_max]
+    sd = torch.from_numpy(scale).to(gpu)
+    hd = torch.from_numpy(shift).to(gpu)
+    rd = rb.to(gpu).contiguous() if res else None
+    y = torch.empty((n, ho, wo, cout), dtype=torch.float32 if out_f32 else torch.bfloat16,
+                    device=gpu)
+    ssn.op_conv_bf16(xd, n, h, w, cin, wd, cout_max, cin_max, k, stride, pad, cout, sd, hd, rd,
+                     act, int(out_f32), y)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy()
+    return got, ref
+
+
+CASES = [
+    # n, h, w, cin, cin_max, cout, cout_max, k, stride
+    (1, 8, 8, 64, 64, 64, 64, 1, 1),        # single tile, one k-block
+    (2, 16, 16, 128, 128, 128, 128, 1, 1),  # M = 512, 2 k-blocks
+    (2, 14, 14, 88, 128, 96, 128, 1, 1),    # channel slices (K tail, N tail)
+    (3, 9, 11, 40, 64, 24, 32, 3, 1),       # 3x3 pad 1, odd spatial, M tail
+    (2, 16, 16, 64, 64, 128, 256, 3, 2),    # 3x3 stride 2
+    (1, 7, 7, 360, 360, 200, 360, 3, 1),    # many k-blocks, cout slice
+    (4, 28, 28, 256, 256, 512, 512, 1, 1),  # bn 256 path (large)
+    (2, 10, 10, 8, 8, 32, 32, 3, 2),        # stem-like cin = 8
+    (64, 1, 1, 2048, 2048, 1000, 1000, 1, 1),  # classifier GEMM
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv_bf16_matches_oracle(gpu, case):
+    n, h, w, cin, cin_max, cout, cout_max, k, stride = case
+    got, ref = _run_bf16(gpu, n, h, w, cin, cin_max, cout, cout_max, k, stride)
+    err = np.abs(got - ref).max() / (np.abs(ref).max() + 1e-6)
+    assert err < 1e-2, f"max rel err {err}"
+
+
+def test_conv_bf16_residual_and_f32_out(gpu):
+    got, ref = _run_bf16(gpu, 2, 12, 12, 64, 64, 64, 64, 1, 1, res=True, act=1)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-2
+    got, ref = _run_bf16(gpu, 8, 1, 1, 256, 512, 1000, 1000, 1, 1, act=0, out_f32=True)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 5e-3
+
+
+def test_conv_bf16_rejects_bad_slices(gpu):
+    import torch
+    x = torch.zeros(64, device=gpu, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        ssn.op_conv_bf16(x, 1, 1, 1, 12, x, 16, 16, 1, 1, 0, 16, y=x)  # cin % 8
+    with pytest.raises(ValueError):
+        ssn.op_conv_bf16(x, 1, 1, 1, 32, x, 16, 16, 1, 1, 0, 16, y=x)  # cin > cin_max
+
+
+@pytest.mark.parametrize("depthwise", [False, True])
+def test_conv_f32_matches_oracle(gpu, depthwise):
+    import torch
+    rng = np.random.default_rng(3)
+    n, h, w = 2, 9, 9
+    cin_max, cout_max, k_max = 24, 24, 5
+    cin, cout, k, stride = (16, 16, 3, 2) if depthwise else (12, 20, 3, 1)
+    x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+    wshape = (cout_max, 1, k_max, k_max) if depthwise else (cout_max, cin_max, k_max, k_max)
+    wmax = rng.standard_normal(wshape).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32)
+    shift = rng.uniform(-0.2, 0.2, cout).astype(np.float32)
+    pad = k // 2
+    ref = O.conv_op(x, wmax, cout_max, cin_max, k_max, k, stride, pad, cout, depthwise=depthwise,
+                    scale=scale, shift=shift, act=1)
+    wk = torch.from_numpy(wmax).permute(0, 2, 3, 1).contiguous().to(gpu)  # KRSC
+    y = torch.empty(ref.shape, dtype=torch.float32, device=gpu)
+    ssn.op_conv_f32(torch.from_numpy(x).to(gpu), n, h, w, cin, wk, cout_max, cin_max, k_max, k,
+                    stride, pad, cout, int(depthwise), torch.from_numpy(scale).to(gpu),
+                    torch.from_numpy(shift).to(gpu), None, 1, y)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-4)
