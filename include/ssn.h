@@ -177,6 +177,13 @@ int ssn_synchronize(ssn_engine* eng, void* stream);
 int ssn_profile_latency(ssn_engine* eng, uint32_t id, uint32_t batch,
                         uint32_t iters, double* median_us);
 
+/* Per-op median device time (µs, CUDA events around each op, ops launched
+ * back to back outside the graphs) of subnet `id` at `batch`; op_us has one
+ * entry per supernet op (ssn_plan_ops order), 0 for skipped ops.  Feeds the
+ * per-kernel roofline accounting. */
+int ssn_profile_ops(ssn_engine* eng, uint32_t id, uint32_t batch,
+                    uint32_t iters, float* op_us, uint32_t n_ops);
+
 int ssn_query(ssn_engine* eng, ssn_stats* out);
 
 /* Device pointer of the engine's last output logits (float32). */

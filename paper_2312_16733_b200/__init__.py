@@ -149,6 +149,7 @@ def lib() -> ctypes.CDLL:
         "ssn_forward": (i32, [P, P, u32, u32, P, P]),
         "ssn_synchronize": (i32, [P, P]),
         "ssn_profile_latency": (i32, [P, u32, u32, u32, ctypes.POINTER(ctypes.c_double)]),
+        "ssn_profile_ops": (i32, [P, u32, u32, u32, P, u32]),
         "ssn_query": (i32, [P, ctypes.POINTER(Stats)]),
         "ssn_device_logits": (i32, [P, ctypes.POINTER(P)]),
         "ssn_last_error": (ctypes.c_char_p, []),
@@ -295,6 +296,14 @@ class Engine:
         check(lib().ssn_profile_latency(self._h, subnet_id, batch, iters, ctypes.byref(us)),
               "profile_latency")
         return us.value
+
+    def profile_ops(self, subnet_id: int, batch: int, iters: int = 5):
+        """Per-op median device µs (ssn_plan_ops order; 0 = skipped op)."""
+        import numpy as np
+        out = np.zeros(512, dtype=np.float32)
+        check(lib().ssn_profile_ops(self._h, subnet_id, batch, iters, out.ctypes.data, 512),
+              "profile_ops")
+        return out
 
     def stats(self) -> dict:
         s = Stats()

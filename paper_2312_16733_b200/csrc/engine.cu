@@ -274,8 +274,12 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
   SSN_THROW(SSN_E_INVALID, "unknown op kind");
 }
 
-// Capture the graph of segment `seg` for LayerSelect variant `mask` at `batch`.
-static void build_graph(ssn_engine* e, int seg, uint32_t mask, uint32_t batch) {
+// Enqueue LayerSelect variant `mask` of segment `seg`: only the blocks the
+// variant runs, with ping-pong buffers so the segment output always lands in
+// the next segment's boundary buffer.  `hook(op, before)` brackets each op.
+template <class Hook>
+static int enqueue_segment(ssn_engine* e, int seg, uint32_t mask, uint32_t batch, cudaStream_t s,
+                           Hook&& hook) {
   const SegmentSpec& S = e->net.segments[seg];
   std::vector<int> act;
   for (int bi : S.blocks) {
@@ -292,20 +296,31 @@ static void build_graph(ssn_engine* e, int seg, uint32_t mask, uint32_t batch) {
   const int k = static_cast<int>(act.size());
   int cur_in = in_bnd;
   int kernels = 0;
+  for (int i = 0; i < k; ++i) {
+    const int out_buf = ((k - 1 - i) % 2 == 0) ? out_bnd : B_P;
+    int map[5];
+    map[S_IN] = cur_in;
+    map[S_OUT] = out_buf;
+    map[S_T1] = B_T1;
+    map[S_T2] = B_T2;
+    map[S_T3] = B_T3;
+    const BlockSpec& b = e->net.blocks[act[i]];
+    for (int q = 0; q < b.count; ++q) {
+      hook(b.first + q, true);
+      kernels += enqueue_op(e, b.first + q, map, batch, s);
+      hook(b.first + q, false);
+    }
+    cur_in = out_buf;
+  }
+  return kernels;
+}
+
+// Capture the graph of segment `seg` for LayerSelect variant `mask` at `batch`.
+static void build_graph(ssn_engine* e, int seg, uint32_t mask, uint32_t batch) {
+  int kernels = 0;
   CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
   try {
-    for (int i = 0; i < k; ++i) {
-      const int out_buf = ((k - 1 - i) % 2 == 0) ? out_bnd : B_P;
-      int map[5];
-      map[S_IN] = cur_in;
-      map[S_OUT] = out_buf;
-      map[S_T1] = B_T1;
-      map[S_T2] = B_T2;
-      map[S_T3] = B_T3;
-      const BlockSpec& b = e->net.blocks[act[i]];
-      for (int q = 0; q < b.count; ++q) kernels += enqueue_op(e, b.first + q, map, batch, e->cap_stream);
-      cur_in = out_buf;
-    }
+    kernels = enqueue_segment(e, seg, mask, batch, e->cap_stream, [](int, bool) {});
   } catch (...) {
     cudaGraph_t g;
     cudaStreamEndCapture(e->cap_stream, &g);
@@ -665,6 +680,50 @@ int ssn_profile_latency(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t ite
     cudaEventDestroy(b);
     std::sort(ms.begin(), ms.end());
     *median_us = ms[ms.size() / 2] * 1000.0;
+  });
+}
+
+int ssn_profile_ops(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t iters, float* op_us,
+                    uint32_t n_ops) {
+  return guarded([&] {
+    if (!e || !op_us || iters == 0) SSN_THROW(SSN_E_INVALID, "bad arguments");
+    if (n_ops < e->net.ops.size()) SSN_THROW(SSN_E_RANGE, "op_us too small");
+    if (batch == 0 || batch > e->desc.max_batch) SSN_THROW(SSN_E_RANGE, "batch out of range");
+    if (ssn_actuate(e, id) != SSN_OK) SSN_THROW(SSN_E_RANGE, g_last_error);
+    const SubnetState& sub = e->subs[id];
+    cudaStream_t s = e->stream;
+    CUDA_TRY(launch_set_row(e->d_rowptr, sub.d_row, s));
+    e->dirty = false;
+    const size_t nop = e->net.ops.size();
+    std::vector<cudaEvent_t> ev(2 * nop);
+    for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
+    std::vector<std::vector<float>> samples(nop);
+    for (uint32_t it = 0; it < iters + 1; ++it) {  // first pass = warm-up
+      std::vector<bool> ran(nop, false);
+      for (size_t si = 0; si < e->net.segments.size(); ++si)
+        enqueue_segment(e, static_cast<int>(si), sub.seg_mask[si], batch, s, [&](int op, bool before) {
+          CUDA_TRY(cudaEventRecord(ev[2 * op + (before ? 0 : 1)], s));
+          ran[op] = true;
+        });
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (it == 0) continue;
+      for (size_t op = 0; op < nop; ++op) {
+        if (!ran[op]) continue;
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, ev[2 * op], ev[2 * op + 1]));
+        samples[op].push_back(ms * 1000.f);
+      }
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
+    for (size_t op = 0; op < nop; ++op) {
+      auto& v = samples[op];
+      if (v.empty()) {
+        op_us[op] = 0.f;
+        continue;
+      }
+      std::sort(v.begin(), v.end());
+      op_us[op] = v[v.size() / 2];
+    }
   });
 }
 

@@ -125,6 +125,7 @@ def plan_cost(desc, cfg: SubnetConfig, elem_bytes: int = 2):
     per = []
     for r in rows:
         if not r["active"]:
+            per.append(None)  # keep per_op aligned with the plan's op index
             continue
         kind = OP_KINDS[r["kind"]]
         hw_in = r["hin"] * r["win"]

@@ -1,0 +1,32 @@
+"""Minimal driver for ncu captures: the bench's sweep step (actuate + forward
+of min/mid/max at one batch), W untimed warm-up steps then S steps."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2312_16733_b200 as ssn  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=64)
+ap.add_argument("--image", type=int, default=224)
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--warmup", type=int, default=1)
+ap.add_argument("--subnets", default="min,mid,max")
+a = ap.parse_args()
+names = a.subnets.split(",")
+desc = ssn.make_desc(ssn.FAMILY_OFA_RESNET50, ssn.DTYPE_BF16, image_size=a.image,
+                     num_classes=1000, max_batch=a.batch, input_format=ssn.INPUT_U8_NHWC)
+eng = ssn.Engine(desc)
+for i, n in enumerate(names):
+    eng.register_subnet(i, ssn.ofa_resnet50_preset(n))
+eng.prepare([a.batch])
+x = torch.randint(0, 256, (a.batch, a.image, a.image, 3), dtype=torch.uint8, device="cuda")
+for it in range(a.warmup + a.steps):
+    for i in range(len(names)):
+        eng.actuate(i)
+        eng.forward(x, a.batch, a.batch, None)
+    eng.synchronize()
+print("kernels per forward:", eng.stats()["last_forward_kernels"])
