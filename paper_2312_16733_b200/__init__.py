@@ -237,9 +237,10 @@ class Engine:
         self.num_classes = desc.num_classes
 
     def close(self):
-        if getattr(self, "_h", None) and self._h.value:
-            lib().ssn_destroy(self._h)
-            self._h = ctypes.c_void_p()
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib_handle is not None:
+            _lib_handle.ssn_destroy(h)
+        self._h = ctypes.c_void_p()
 
     __del__ = close
 

@@ -30,9 +30,9 @@
 #include "supernet.hpp"
 
 namespace ssn {
-int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int bn);
+int make_weight_maps(TcMaps* maps, const void* w, int cin_store, int taps, int cout, int bn);
 int choose_bn(int cout_max, long M);
-cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& map, cudaStream_t s);
+cudaError_t launch_conv_tc(const ConvParams& p, const TcMaps& maps, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t launch_input(const InputParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
@@ -106,8 +106,6 @@ struct ssn_engine {
   bool bf16 = true;
   uint8_t* d_w = nullptr;
   std::vector<std::vector<float>> gamma, beta;  // host copies for SubnetNorm folding
-  std::vector<CUtensorMap> tmaps;  // per op (tcgen05 convs)
-  std::vector<int> op_bn;
   std::vector<SubnetState> subs;
   const OpDesc** d_rowptr = nullptr;
   int active = -1;
@@ -260,8 +258,8 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.depthwise = o.depthwise;
       if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M);
-        CUtensorMap map_{};
-        if (make_weight_map(&map_, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
+        TcMaps map_{};
+        if (make_weight_maps(&map_, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
         CUDA_TRY(launch_conv_tc(p, map_, s));
       } else {
@@ -803,8 +801,8 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.res_post = 0;
     p.out_f32 = out_f32;
     p.bn = choose_bn(cout_max, p.M);
-    CUtensorMap map{};
-    if (make_weight_map(&map, wgt, cin_max, k * k, cout_max, p.bn) != 0)
+    TcMaps map{};
+    if (make_weight_maps(&map, wgt, cin_max, k * k, cout_max, p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
     CUDA_TRY(launch_conv_tc(p, map, s));
   });

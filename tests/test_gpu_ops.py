@@ -66,6 +66,14 @@ CASES = [
     (4, 28, 28, 256, 256, 512, 512, 1, 1),  # bn 256 path (large)
     (2, 10, 10, 8, 8, 32, 32, 3, 2),        # stem-like cin = 8
     (64, 1, 1, 2048, 2048, 1000, 1000, 1, 1),  # classifier GEMM
+    # packed-tap K blocks (cin_a <= 32, full kernel): cslot 16 / 32 with a channel gap
+    (4, 16, 16, 16, 16, 32, 32, 3, 1),
+    (2, 20, 20, 24, 32, 32, 64, 3, 2),
+    (3, 15, 15, 32, 32, 40, 48, 3, 1),
+    # persistent schedule: more tiles than SMs, several n tiles
+    (64, 28, 28, 128, 128, 128, 128, 1, 1),
+    (8, 14, 14, 256, 256, 1024, 1024, 1, 1),
+    (16, 14, 14, 104, 128, 360, 360, 3, 1),
 ]
 
 
