@@ -6,28 +6,30 @@
 //   PAPER.md:472-481 SubnetNorm folded into the epilogue).
 //
 // Design:
-//  * Persistent, warp-specialised: one CTA per SM walks a static tile
-//    schedule.  Warps 0-3 produce operands, warp 12 issues tcgen05.mma,
-//    warps 4-11 drain the accumulator.  The accumulator is double-buffered in
-//    TMEM (2 x BN_MAX fp32 columns), so tile i's epilogue overlaps tile i+1's
-//    mainloop, and the smem ring runs continuously across tiles.
-//  * B operand (weights) — the max-shape KRSC tensor is stored ONCE; TMA
-//    tensor maps over [cout_max][k_max^2][cin_max] load boxes of its LEADING
-//    slice straight into 128B-swizzled shared memory, never a copy.  Normal
-//    mode: box {64 ch, 1 tap, bn}.  Packed-tap mode (small cin_a, full
-//    kernel): box {cslot, 64/cslot taps, bn} so one 64-wide K block spans
-//    several taps instead of wasting most of it on zero channels.
-//  * A operand (activations) — compact NHWC with cin_a channels (a
-//    subnet-dependent stride), gathered by 128 producer threads with 16-byte
-//    cp.async (zero-fill for padding / M tail / channel tail) directly into
-//    the same SW128 K-major layout; cp.async.wait_group + fence.proxy.async +
-//    mbarrier hand it to the tensor core.
-//  * Epilogue: tcgen05.ld 32 lanes x 32 columns, SubnetNorm scale/shift,
-//    residual (prefetched before the TMEM load), ReLU, bf16 / fp32 store.
-//  * Subnet extents (cin_a, cout_a, k_a, SubnetNorm row) come from the
-//    actuated subnet's device descriptor, so one graph-captured launch serves
-//    every subnet; the tile count is derived from cout_a on the device.
+//  * Both operands move by TMA, issued by ONE producer thread per CTA:
+//      A (activations): TMA im2col mode — one cp.async.bulk.tensor.4d.im2col
+//        per K block loads 128 consecutive output pixels x 64 channels of one
+//        filter tap; padding, channel tails (> cin_a) and the batch tail are
+//        TMA zero fill.  The map is per (subnet, op): it encodes the subnet's
+//        compact activation layout (cin_a-channel stride) and lives in the
+//        actuated subnet's device OpDesc row, read in place by the TMA unit.
+//      B (weights): the max-shape KRSC tensor is stored ONCE; a 3-D tiled map
+//        over [cout_max][k_max^2][cin_max] loads {64 ch, 1 tap, bn} boxes of
+//        its LEADING slice — no copy of any slice ever exists.
+//    Both land 128B-swizzled (SW128 K-major), the layout tcgen05.mma reads.
+//  * Persistent and warp-specialised: one CTA per SM walks a static tile
+//    schedule; warp 0 produces, warp 9 issues tcgen05.mma (one thread), warps
+//    1-8 drain.  Accumulators live in a TMEM ring (NACC buffers of BN_MAX fp32
+//    columns), so several tiles are in flight between MMA and epilogue.
+//  * Epilogue: two groups of 4 warps take alternate tiles; each warp
+//    tcgen05.ld's 32 TMEM lanes x 32 columns, transposes through padded smem,
+//    then applies SubnetNorm scale/shift, residual and ReLU on coalesced
+//    64-byte row segments and stores bf16 (or fp32 logits).
+//  * Subnet extents (cin_a, cout_a, k_a, SubnetNorm row, activation map) come
+//    from the actuated subnet's descriptor, so one graph-captured launch
+//    serves every subnet; the tile count follows cout_a on the device.
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -35,34 +37,29 @@ namespace ssn {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
-constexpr int TC_PROD_WARPS = 4;
 constexpr int TC_EPI_WARPS = 8;
-constexpr int TC_MMA_WARP = TC_PROD_WARPS + TC_EPI_WARPS;  // 12
-constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;          // 416
+constexpr int TC_PROD_WARP = 0;
+constexpr int TC_MMA_WARP = 1 + TC_EPI_WARPS;   // 9
+constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 320
 constexpr int TC_STG_LD = 36;  // padded fp32 row of the 32x32 epilogue transpose tile
 constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
-
 
 template <int BN_MAX, int STAGES>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN_MAX * TC_BK * 2;
+  // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
+  // (max 4), so the MMA can run several tiles ahead of the epilogue.
+  static constexpr int NACC = 512 / BN_MAX > 4 ? 4 : 512 / BN_MAX;
   static constexpr int SMEM =
-      1024 + STAGES * (A_BYTES + B_BYTES) + TC_STG_BYTES + (2 * STAGES + 4) * 8 + 16;
+      1024 + STAGES * (A_BYTES + B_BYTES) + TC_STG_BYTES + (2 * STAGES + 2 * NACC) * 8 + 16;
 };
-
-__device__ __forceinline__ int cslot_for(int cin, int k, int k_max) {
-  if (k != k_max || k == 1) return 64;
-  if (cin <= 8) return 8;
-  if (cin <= 16) return 16;
-  if (cin <= 32) return 32;
-  return 64;
-}
 
 template <int BN_MAX, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ TcMaps maps) {
+    conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
   using C = TcCfg<BN_MAX, STAGES>;
+  constexpr int NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -71,11 +68,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   float* epi_stage = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES + TC_STG_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + STAGES;  // [NACC]
+  uint64_t* tempty = tfull + NACC;   // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
 
-  const OpDesc d = load_desc(p.row, p.fixed, p.op);
+  const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
+  const OpDims d = load_desc(p.row, p.fixed, p.op);
   const int bn = p.bn;
   const int mt = (p.M + TC_BM - 1) / TC_BM;
   const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
@@ -84,90 +82,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
-  const int cslot = cslot_for(d.cin, ka, p.k_max);
-  const bool packed = cslot < 64;
-  const int tpk = 64 / cslot;  // taps per K block in packed mode
   const int cblocks = (d.cin + TC_BK - 1) / TC_BK;
-  const int nk = packed ? (ka * ka + tpk - 1) / tpk : ka * ka * cblocks;
-  const CUtensorMap* wmap = &maps.w[cslot == 64 ? 0 : cslot == 32 ? 1 : cslot == 16 ? 2 : 3];
+  const int nk = ka * ka * cblocks;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], TC_PROD_WARPS * 32 + 1);  // producers + expect_tx arrival
+      mbar_init(&full[s], 1);  // the producer's expect_tx arrival
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], TC_EPI_WARPS);
+      mbar_init(&tempty[a], TC_EPI_WARPS / 2);  // the 4 warps of the owning group
     }
     fence_mbar_init();
-    tma_prefetch(wmap);
+    tma_prefetch(&wmap);
+    tma_prefetch(&dp->amap);
   }
-  if (warp == TC_MMA_WARP) tmem_alloc(tmem_slot, 2 * BN_MAX);
+  if (warp == TC_MMA_WARP) tmem_alloc(tmem_slot, NACC * BN_MAX);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < TC_PROD_WARPS) {
-    // ============================================================ producers
-    const int j = lane & 7;      // 16-byte chunk within the 128-byte K row
-    const int rsub = lane >> 3;  // 0..3
-    const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
-    const uint32_t a_base = smem_u32(sA);
-    const int hwo = p.ho * p.wo;
-    const uint32_t tx_bytes = static_cast<uint32_t>(bn * TC_BK * 2);
-    // packed mode: this thread's chunk is channel slot (j*8) % cslot of tap (j*8)/cslot
-    const int pk_tap = (j * 8) / cslot, pk_c = (j * 8) % cslot;
-    int g = 0;  // global K-block counter (ring position)
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t / nt) * TC_BM;
-      const int n0 = (t % nt) * bn;
-      int pix[8], ih0[8], iw0[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = m0 + warp * 32 + rsub + 4 * i;
-        if (m < p.M) {
-          const int img = m / hwo;
-          const int rem = m - img * hwo;
-          const int oh = rem / p.wo;
-          const int ow = rem - oh * p.wo;
-          pix[i] = img * p.h * p.w_;
-          ih0[i] = oh * p.stride - pad;
-          iw0[i] = ow * p.stride - pad;
-        } else {
-          pix[i] = 0;
-          ih0[i] = -(1 << 20);
-          iw0[i] = -(1 << 20);
-        }
-      }
-      int tr = 0, ts = 0, cb = 0;  // normal mode iteration state
-      for (int kb = 0; kb < nk; ++kb, ++g) {
-        const int s = g % STAGES;
-        const uint32_t ph = (g / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        int r, q, c;
-        bool cok;
-        if (packed) {
-          const int tap = kb * tpk + pk_tap;
-          r = tap / ka;
-          q = tap - r * ka;
-          c = pk_c;
-          cok = tap < ka * ka && c < d.cin;
-          if (tid == 0) {
-            mbar_arrive_expect_tx(&full[s], tx_bytes);
-            tma_load_4d(sB + s * C::B_BYTES, wmap, &full[s], 0, n0, 0, kb * tpk);
-          }
-        } else {
-          r = tr;
-          q = ts;
-          c = cb * TC_BK + j * 8;
-          cok = c < d.cin;
-          if (tid == 0) {
-            mbar_arrive_expect_tx(&full[s], tx_bytes);
-            tma_load_3d(sB + s * C::B_BYTES, wmap, &full[s], cb * TC_BK,
-                        (tr + koff) * p.k_max + (ts + koff), n0);
-          }
+  if (warp == TC_PROD_WARP) {
+    // ============================================================ producer
+    if (lane == 0) {
+      const CUtensorMap* amap = &dp->amap;
+      const int hwo = p.ho * p.wo;
+      const uint32_t tx = static_cast<uint32_t>(C::A_BYTES + bn * TC_BK * 2);
+      int g = 0;  // global K-block counter (ring position)
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / nt) * TC_BM;
+        const int n0 = (t % nt) * bn;
+        const int img = m0 / hwo;
+        const int rem = m0 - img * hwo;
+        const int oh = rem / p.wo;
+        const int ow = rem - oh * p.wo;
+        const int w0 = ow * p.stride - pad, h0 = oh * p.stride - pad;
+        int tr = 0, ts = 0, cb = 0;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], tx);
+          tma_im2col_4d(sA + s * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0, img,
+                        static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
+          tma_load_3d(sB + s * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
+                      (tr + koff) * p.k_max + (ts + koff), n0);
           if (++cb == cblocks) {
             cb = 0;
             if (++ts == ka) {
@@ -176,63 +137,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
         }
-        const uint32_t dst = a_base + s * C::A_BYTES;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = warp * 32 + rsub + 4 * i;
-          const int ih = ih0[i] + r, iw = iw0[i] + q;
-          const bool ok = cok && static_cast<unsigned>(ih) < static_cast<unsigned>(p.h) &&
-                          static_cast<unsigned>(iw) < static_cast<unsigned>(p.w_);
-          const __nv_bfloat16* src =
-              ok ? x + (static_cast<size_t>(pix[i] + ih * p.w_ + iw) * d.cin + c) : x;
-          cp_async_16(dst + row * 128 + ((j ^ (row & 7)) << 4), src, ok ? 16u : 0u);
-        }
-        // decoupled: the barrier completes when this thread's copies land, so
-        // all STAGES slots can be in flight and the producer never stalls on
-        // its own loads (the CUTLASS sm100 cp.async pipeline contract)
-        cp_async_arrive_noinc(&full[s]);
       }
     }
+    __syncwarp();
   } else if (warp < TC_MMA_WARP) {
     // ============================================================ epilogue
     // TMEM gives each thread one ROW; global memory wants each warp to touch
     // whole row segments.  Each 32x32 fp32 chunk is transposed through a
     // per-warp padded smem tile: afterwards lane (rsub = lane/4, seg = lane%4)
     // owns 8 consecutive columns of rows rsub, rsub+8, ... so residual loads
-    // and output stores are 64-byte row-contiguous and coalesced.
-    const int ew = warp - TC_PROD_WARPS;
-    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    const int half = ew >> 2;      // column interleave
+    // and output stores are 64-byte row-contiguous and coalesced.  Two groups
+    // (4 warps each, one per TMEM lane quarter) take alternate tiles.
+    const int ew = warp - 1;
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warps 1-4, 5-8)
+    const int group = ew >> 2;     // tile parity this warp drains
     float* stg = epi_stage + ew * (32 * TC_STG_LD);
     const int seg = lane & 3, rsub = lane >> 2;
     const float* scale = d.scale;
     const float* shift = d.shift;
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      const int a = i & 1;
-      const uint32_t use = static_cast<uint32_t>(i >> 1);
+      if ((i & 1) != group) continue;
+      const int a = i % NACC;
+      const uint32_t use = static_cast<uint32_t>(i / NACC);
       const int m0 = (t / nt) * TC_BM + quarter * 32;
       const int n0 = (t % nt) * bn;
-      mbar_wait(&tfull[a], use & 1);
-      tc_fence_after();
-      for (int cc = half * 32; cc < bn; cc += 64) {
+      for (int cc = 0; cc < bn; cc += 32) {
         if (n0 + cc >= d.cout) break;  // warp-uniform
-        float v[32];
-        tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
-        float4* srow = reinterpret_cast<float4*>(stg + lane * TC_STG_LD);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          srow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        __syncwarp();
+        // everything that does not depend on the accumulator is issued first
         const int col = n0 + cc + seg * 8;
-        if (col < d.cout && cc + seg * 8 < bn) {
-          float sc[8], sh[8];
+        const bool colok = col < d.cout && cc + seg * 8 < bn;
+        float sc[8], sh[8];
+        uint4 rv[4];
+        if (colok) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             sc[q] = scale ? __ldg(scale + col + q) : 1.f;
             sh[q] = shift ? __ldg(shift + col + q) : 0.f;
           }
-          uint4 rv[4];
           if (p.res) {
 #pragma unroll
             for (int r4 = 0; r4 < 4; ++r4) {
@@ -242,6 +184,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col));
             }
           }
+        }
+        if (cc == 0) {
+          mbar_wait(&tfull[a], use & 1);
+          tc_fence_after();
+        }
+        float v[32];
+        tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+        float4* srow = reinterpret_cast<float4*>(stg + lane * TC_STG_LD);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          srow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
+        if (colok) {
 #pragma unroll
           for (int r4 = 0; r4 < 4; ++r4) {
             const int rr = rsub + 8 * r4;
@@ -302,8 +257,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       int g = 0, i = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-        const int a = i & 1;
-        const uint32_t use = static_cast<uint32_t>(i >> 1);
+        const int a = i % NACC;
+        const uint32_t use = static_cast<uint32_t>(i / NACC);
         mbar_wait(&tempty[a], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t acc = tmem + a * BN_MAX;
@@ -311,18 +266,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int s = g % STAGES;
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&full[s], ph);
-          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 reads
           tc_fence_after();
           const uint64_t ad = umma_desc_sw128(a0 + s * C::A_BYTES);
-          // packed-tap B tiles use the no-swizzle core-matrix layout written
-          // by the 4-D TMA map: K chunks of 8 are bn*16 bytes apart.
-          const uint64_t bd = packed ? umma_desc_noswz(b0 + s * C::B_BYTES, bn * 16, 128)
-                                     : umma_desc_sw128(b0 + s * C::B_BYTES);
-          const uint64_t bstep = packed ? static_cast<uint64_t>(2 * bn) : 2u;  // 16B units / K=16
+          const uint64_t bd = umma_desc_sw128(b0 + s * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk)
-            tc_mma_bf16(acc, ad + static_cast<uint64_t>(kk * 2), bd + kk * bstep, idesc,
-                        (kb | kk) != 0 ? 1u : 0u);
+            tc_mma_bf16(acc, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2),
+                        idesc, (kb | kk) != 0 ? 1u : 0u);
           tc_commit(&empty[s]);
         }
         tc_commit(&tfull[a]);
@@ -334,7 +284,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == TC_MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem, 2 * BN_MAX);
+    tmem_dealloc(tmem, NACC * BN_MAX);
   }
 }
 
@@ -345,59 +295,64 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
-  return fn;
+template <class F>
+static F driver_fn(const char* name) {
+  void* ptr = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<F>(ptr);
+  return nullptr;
 }
 
-// Tensor maps over a max-shape KRSC bf16 weight tensor [cout][taps][cin_store]:
-// boxes {cslot, 64/cslot, bn} for cslot = 64, 32, 16, 8, 128B swizzle.
-int make_weight_maps(TcMaps* maps, const void* w, int cin_store, int taps, int cout, int bn) {
-  EncodeTiledFn enc = get_encode();
+// B operand: map over a max-shape KRSC bf16 weight tensor [cout][taps][cin_store]
+// with {64 ch, 1 tap, bn} boxes, 128B swizzle.
+int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int bn) {
+  static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
   if (!enc) return -1;
-  // normal mode: {64 ch, 1 tap, bn} boxes, 128B swizzle (SW128 K-major tile)
-  {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin_store), static_cast<cuuint64_t>(taps),
-                          static_cast<cuuint64_t>(cout)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(cin_store) * 2,
-                             static_cast<cuuint64_t>(taps) * cin_store * 2};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(TC_BK), 1, static_cast<cuuint32_t>(bn)};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(&maps->w[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims,
-                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return -static_cast<int>(r);
-  }
-  // packed-tap modes: the same tensor viewed as (c8, n, c/8, tap) so a box
-  // {8, bn, cslot/8, 64/cslot} lands as no-swizzle K-major core matrices
-  // ([K chunk][n][8 ch]), K order = tap-major then channel — matching A.
-  const int slots[3] = {32, 16, 8};
-  for (int i = 0; i < 3; ++i) {
-    const int cs = slots[i];
-    cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(cout),
-                          static_cast<cuuint64_t>((cin_store + 7) / 8),
-                          static_cast<cuuint64_t>(taps)};
-    cuuint64_t strides[3] = {static_cast<cuuint64_t>(taps) * cin_store * 2, 16,
-                             static_cast<cuuint64_t>(cin_store) * 2};
-    cuuint32_t box[4] = {8, static_cast<cuuint32_t>(bn), static_cast<cuuint32_t>(cs / 8),
-                         static_cast<cuuint32_t>(64 / cs)};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(&maps->w[1 + i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(w),
-                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return -static_cast<int>(r);
-  }
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin_store), static_cast<cuuint64_t>(taps),
+                        static_cast<cuuint64_t>(cout)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cin_store) * 2,
+                           static_cast<cuuint64_t>(taps) * cin_store * 2};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(TC_BK), 1, static_cast<cuuint32_t>(bn)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
+}
+
+// A operand: im2col map over a compact NHWC bf16 activation [n][h][w][cin]
+// for a k x k / stride / pad convolution: 128 pixels x 64 channels per load.
+int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
+                 int pad) {
+  static EncodeIm2colFn enc = driver_fn<EncodeIm2colFn>("cuTensorMapEncodeIm2col");
+  if (!enc) return -1;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
+                        static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(cin) * 2,
+                           static_cast<cuuint64_t>(w) * cin * 2,
+                           static_cast<cuuint64_t>(h) * w * cin * 2};
+  const int lower[2] = {-pad, -pad};
+  const int upper[2] = {pad - (k - 1), pad - (k - 1)};
+  cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
+                   lower, upper, TC_BK, TC_BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -static_cast<int>(r);
+  // Same driver workaround CUTLASS applies to im2col maps of tensors < 128 KB
+  // on drivers <= 13.1 (cute/atom/copy_traits_sm90_im2col.hpp).
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  const unsigned long long bytes = 2ull * n * h * w * cin;
+  if (drv <= 13010 && bytes < 131072ull) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   return 0;
 }
 
@@ -444,18 +399,18 @@ cudaError_t init_conv_tc() {
 }
 
 template <int BN_MAX, int STAGES>
-static cudaError_t launch_impl(const ConvParams& p, const TcMaps& maps, cudaStream_t s) {
+static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
   using C = TcCfg<BN_MAX, STAGES>;
   const long tiles = static_cast<long>((p.M + TC_BM - 1) / TC_BM) * ((p.cout_max + p.bn - 1) / p.bn);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  conv_tc_kernel<BN_MAX, STAGES><<<grid, TC_THREADS, C::SMEM, s>>>(p, maps);
+  conv_tc_kernel<BN_MAX, STAGES><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv_tc(const ConvParams& p, const TcMaps& maps, cudaStream_t s) {
-  if (p.bn <= 64) return launch_impl<64, 7>(p, maps, s);
-  if (p.bn <= 128) return launch_impl<128, 5>(p, maps, s);
-  return launch_impl<256, 3>(p, maps, s);
+cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
+  if (p.bn <= 64) return launch_impl<64, 7>(p, wmap, s);
+  if (p.bn <= 128) return launch_impl<128, 5>(p, wmap, s);
+  return launch_impl<256, 3>(p, wmap, s);
 }
 
 }  // namespace ssn

@@ -13,7 +13,11 @@ namespace ssn {
 // SubnetNorm row of the ACTUATED subnet.  Kernels read it at run time through
 // a device word that ssn_actuate() re-points, so CUDA-graph segments never
 // need re-instantiation when the subnet changes.
-struct OpDesc {
+struct alignas(64) OpDesc {
+  // TMA im2col map over this op's input activation as THIS subnet lays it out
+  // (compact NHWC, cin_a channels; bf16 tcgen05 convs only).  64-byte aligned
+  // in global memory so the TMA unit can use it in place.
+  CUtensorMap amap;
   int cin;             // active input channels (WeightSlice)
   int cout;            // active output channels
   int k;               // active kernel size (centre crop of k_max)
@@ -38,11 +42,6 @@ struct ConvParams {
   int bn;             // N tile (tcgen05 path)
 };
 
-// TMA maps over one max-shape weight tensor for the tcgen05 conv:
-// cslot = 64, 32, 16, 8 channels x (64 / cslot) taps x bn output rows.
-struct TcMaps {
-  CUtensorMap w[4];
-};
 
 struct PoolParams {
   const void* x;
@@ -60,11 +59,25 @@ struct InputParams {
   int format;   // ssn_input_format
   int cpad;     // output channels (3 f32 / 8 bf16)
   int out_bf16;
+  int im2col_k;           // > 0: emit the k x k / stride im2col (bf16, cpad channels)
+  int im2col_stride;
+  int ho, wo;
 };
 
-__device__ __forceinline__ OpDesc load_desc(const OpDesc* const* row, const OpDesc* fixed, int op) {
-  const OpDesc* r = fixed ? fixed : (*row + op);
-  return *r;
+struct OpDims {
+  int cin, cout, k, pad;
+  const float* scale;
+  const float* shift;
+};
+
+__device__ __forceinline__ const OpDesc* desc_ptr(const OpDesc* const* row, const OpDesc* fixed,
+                                                  int op) {
+  return fixed ? fixed : (*row + op);
+}
+
+__device__ __forceinline__ OpDims load_desc(const OpDesc* const* row, const OpDesc* fixed, int op) {
+  const OpDesc* r = desc_ptr(row, fixed, op);
+  return OpDims{r->cin, r->cout, r->k, r->pad, r->scale, r->shift};
 }
 
 // ---------------------------------------------------------------------------
@@ -123,6 +136,19 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
       "r"(c3)
+      : "memory");
+}
+
+// TMA im2col: pixelsPerColumn output pixels x channelsPerPixel channels of
+// filter tap (off_w, off_h), starting at input coordinate (c, w, h, n).
+__device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                              int c, int w, int h, int n, uint16_t off_w,
+                                              uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(off_w), "h"(off_h)
       : "memory");
 }
 

@@ -30,9 +30,11 @@
 #include "supernet.hpp"
 
 namespace ssn {
-int make_weight_maps(TcMaps* maps, const void* w, int cin_store, int taps, int cout, int bn);
+int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int bn);
+int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
+                 int pad);
 int choose_bn(int cout_max, long M);
-cudaError_t launch_conv_tc(const ConvParams& p, const TcMaps& maps, cudaStream_t s);
+cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t launch_input(const InputParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
@@ -160,7 +162,11 @@ static void generate_blob(const Net& net, uint8_t* blob) {
             const uint64_t idx = ((static_cast<uint64_t>(o) * t.cin + i) * t.k + r) * t.k + s;
             const float v = ssn_weight_value(seed, static_cast<uint32_t>(ti), idx, t.fan_in, bf16);
             // storage: KRSC [cout][k][k][cin_store] (depthwise: [c][k][k])
-            const uint64_t e = (static_cast<uint64_t>(o) * kk + r * t.k + s) * t.cin_store + i;
+            // im2col stem: [cout][(r*k+s)*cin + c] padded to cin_store
+            const uint64_t e =
+                t.im2col_stem
+                    ? static_cast<uint64_t>(o) * t.cin_store + (r * t.k + s) * t.cin + i
+                    : (static_cast<uint64_t>(o) * kk + r * t.k + s) * t.cin_store + i;
             if (bf16) {
               reinterpret_cast<uint16_t*>(blob + t.w_off)[e] = ssn_f32_to_bf16_bits(v);
             } else {
@@ -208,6 +214,12 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.format = static_cast<int>(e->desc.input_format);
       p.cpad = o.cout_max;
       p.out_bf16 = bf;
+      if (o.hout != o.hin) {  // fused stem im2col (bf16 OFA-ResNet50)
+        p.im2col_k = o.k_max;
+        p.im2col_stride = o.stride;
+      }
+      p.ho = o.hout;
+      p.wo = o.wout;
       CUDA_TRY(launch_input(p, s));
       return 1;
     }
@@ -258,10 +270,10 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.depthwise = o.depthwise;
       if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M);
-        TcMaps map_{};
-        if (make_weight_maps(&map_, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
+        CUtensorMap wmap{};
+        if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
-        CUDA_TRY(launch_conv_tc(p, map_, s));
+        CUDA_TRY(launch_conv_tc(p, wmap, s));
       } else {
         if (bf) SSN_THROW(SSN_E_INVALID, "bf16 depthwise conv not supported for this family");
         CUDA_TRY(launch_conv_f32(p, s));
@@ -275,9 +287,15 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
 // Enqueue LayerSelect variant `mask` of segment `seg`: only the blocks the
 // variant runs, with ping-pong buffers so the segment output always lands in
 // the next segment's boundary buffer.  `hook(op, before)` brackets each op.
-template <class Hook>
-static int enqueue_segment(ssn_engine* e, int seg, uint32_t mask, uint32_t batch, cudaStream_t s,
-                           Hook&& hook) {
+struct SlotMap {
+  int op;
+  int map[5];
+};
+
+// The ops one LayerSelect variant of a segment runs, each with its slot ->
+// arena-buffer mapping (used by graph capture AND by ssn_register_subnet to
+// encode each op's activation TMA map over the buffer it will really read).
+static std::vector<SlotMap> segment_plan(const ssn_engine* e, int seg, uint32_t mask) {
   const SegmentSpec& S = e->net.segments[seg];
   std::vector<int> act;
   for (int bi : S.blocks) {
@@ -293,22 +311,33 @@ static int enqueue_segment(ssn_engine* e, int seg, uint32_t mask, uint32_t batch
   const int out_bnd = seg % 2 == 0 ? B_BND1 : B_BND0;
   const int k = static_cast<int>(act.size());
   int cur_in = in_bnd;
-  int kernels = 0;
+  std::vector<SlotMap> out;
   for (int i = 0; i < k; ++i) {
     const int out_buf = ((k - 1 - i) % 2 == 0) ? out_bnd : B_P;
-    int map[5];
-    map[S_IN] = cur_in;
-    map[S_OUT] = out_buf;
-    map[S_T1] = B_T1;
-    map[S_T2] = B_T2;
-    map[S_T3] = B_T3;
+    SlotMap sm{};
+    sm.map[S_IN] = cur_in;
+    sm.map[S_OUT] = out_buf;
+    sm.map[S_T1] = B_T1;
+    sm.map[S_T2] = B_T2;
+    sm.map[S_T3] = B_T3;
     const BlockSpec& b = e->net.blocks[act[i]];
     for (int q = 0; q < b.count; ++q) {
-      hook(b.first + q, true);
-      kernels += enqueue_op(e, b.first + q, map, batch, s);
-      hook(b.first + q, false);
+      sm.op = b.first + q;
+      out.push_back(sm);
     }
     cur_in = out_buf;
+  }
+  return out;
+}
+
+template <class Hook>
+static int enqueue_segment(ssn_engine* e, int seg, uint32_t mask, uint32_t batch, cudaStream_t s,
+                           Hook&& hook) {
+  int kernels = 0;
+  for (const SlotMap& sm : segment_plan(e, seg, mask)) {
+    hook(sm.op, true);
+    kernels += enqueue_op(e, sm.op, sm.map, batch, s);
+    hook(sm.op, false);
   }
   return kernels;
 }
@@ -372,10 +401,27 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     CUDA_TRY(cudaMalloc(&st.d_norm, st.norm_bytes));
     CUDA_TRY(cudaMemcpy(st.d_norm, norm.data(), st.norm_bytes, cudaMemcpyHostToDevice));
   }
+  st.seg_mask.assign(e->net.segments.size(), 0);
+  for (size_t si = 0; si < e->net.segments.size(); ++si)
+    for (size_t f = 0; f < e->net.segments[si].flags.size(); ++f)
+      if (cfg.depth[e->net.segments[si].flags[f]]) st.seg_mask[si] |= 1u << f;
+  // physical input buffer of every op this subnet runs
+  std::vector<const void*> in_ptr(st.plan.ops.size(), nullptr);
+  for (size_t si = 0; si < e->net.segments.size(); ++si)
+    for (const SlotMap& sm : segment_plan(e, static_cast<int>(si), st.seg_mask[si]))
+      in_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in, sm.map);
   std::vector<OpDesc> row(st.plan.ops.size());
   for (size_t oi = 0; oi < st.plan.ops.size(); ++oi) {
     const OpSpec& o = st.plan.ops[oi];
     OpDesc& dsc = row[oi];
+    std::memset(&dsc, 0, sizeof(dsc));
+    if (e->bf16 && o.active && (o.kind == OP_CONV || o.kind == OP_LINEAR) && !o.depthwise) {
+      // WeightSlice A operand: im2col TMA map over this subnet's compact
+      // activation (cin_a channels) in the buffer its graph variant reads.
+      if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin, o.win,
+                       o.cin, o.k, o.stride, o.k / 2) != 0)
+        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed for op " + std::to_string(oi));
+    }
     dsc.cin = o.cin;
     dsc.cout = o.cout;
     dsc.k = o.k;
@@ -391,10 +437,6 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
   }
   CUDA_TRY(cudaMalloc(&st.d_row, row.size() * sizeof(OpDesc)));
   CUDA_TRY(cudaMemcpy(st.d_row, row.data(), row.size() * sizeof(OpDesc), cudaMemcpyHostToDevice));
-  st.seg_mask.assign(e->net.segments.size(), 0);
-  for (size_t si = 0; si < e->net.segments.size(); ++si)
-    for (size_t f = 0; f < e->net.segments[si].flags.size(); ++f)
-      if (cfg.depth[e->net.segments[si].flags[f]]) st.seg_mask[si] |= 1u << f;
   st.ok = true;
   if (id >= e->subs.size()) e->subs.resize(id + 1);
   SubnetState& old = e->subs[id];
@@ -462,6 +504,11 @@ int ssn_plan_ops(const ssn_supernet_desc* desc, const ssn_subnet_cfg* c, ssn_op_
       r.k = static_cast<uint32_t>(o.kind == OP_AVGPOOL ? o.pool_k : o.k);
       r.stride = static_cast<uint32_t>(o.stride);
       r.hin = o.hin; r.win = o.win; r.hout = o.hout; r.wout = o.wout;
+      if (o.tensor >= 0 && net.tensors[o.tensor].im2col_stem) {
+        // report the logical convolution (3x3 s2 over 3 channels), not its GEMM form
+        r.k = 3; r.stride = 2; r.cin = r.cin_max = 3;
+        r.hin = r.win = net.ops[0].hin;
+      }
       r.cin = o.cin; r.cout = o.cout; r.cin_max = o.cin_max; r.cout_max = o.cout_max;
       r.depthwise = o.depthwise;
       r.block = static_cast<uint32_t>(blk[i]);
@@ -755,6 +802,19 @@ int ssn_device_logits(ssn_engine* e, const float** out) {
 
 // ---- operator-level entry points -----------------------------------------
 
+static OpDesc plain_desc(int cin, int cout, int k, int pad, const float* scale,
+                         const float* shift) {
+  OpDesc d;
+  std::memset(&d, 0, sizeof(d));
+  d.cin = cin;
+  d.cout = cout;
+  d.k = k;
+  d.pad = pad;
+  d.scale = scale;
+  d.shift = shift;
+  return d;
+}
+
 static OpDesc* op_desc_scratch(const OpDesc& d, cudaStream_t s) {
   static OpDesc* dev = nullptr;
   static std::mutex mu;
@@ -779,7 +839,9 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     if (k < 1 || stride < 1 || pad < 0) SSN_THROW(SSN_E_INVALID, "bad geometry");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(init_conv_tc());
-    OpDesc d{cin, cout, k, pad, scale, shift};
+    OpDesc d = plain_desc(cin, cout, k, pad, scale, shift);
+    if (make_act_map(&d.amap, x, n, h, w, cin, k, stride, pad) != 0)
+      SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed");
     ConvParams p{};
     p.x = x;
     p.y = y;
@@ -801,10 +863,10 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.res_post = 0;
     p.out_f32 = out_f32;
     p.bn = choose_bn(cout_max, p.M);
-    TcMaps map{};
-    if (make_weight_maps(&map, wgt, cin_max, k * k, cout_max, p.bn) != 0)
+    CUtensorMap wmap{};
+    if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
-    CUDA_TRY(launch_conv_tc(p, map, s));
+    CUDA_TRY(launch_conv_tc(p, wmap, s));
   });
 }
 
@@ -817,7 +879,7 @@ int ssn_op_conv_f32(const float* x, int n, int h, int w, int cin, const float* w
     if (cin > cin_max || cout > cout_max || k > k_max || (depthwise && cin != cout))
       SSN_THROW(SSN_E_INVALID, "active slice exceeds the max shape");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    OpDesc d{cin, cout, k, pad, scale, shift};
+    OpDesc d = plain_desc(cin, cout, k, pad, scale, shift);
     ConvParams p{};
     p.x = x;
     p.y = y;

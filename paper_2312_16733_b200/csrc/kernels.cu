@@ -46,6 +46,56 @@ __global__ void input_kernel(InputParams p) {
   }
 }
 
+// Input staging fused with the stem conv's im2col (bf16): output pixel
+// (n, oh, ow) gets the k*k*3 input values (r, s, c) of its window, zero
+// padded, then zeros up to cpad (a multiple of 8) — a K = cpad GEMM operand.
+__global__ void input_im2col_kernel(InputParams p) {
+  const long npix = static_cast<long>(p.n) * p.ho * p.wo;
+  const int k = p.im2col_k, st = p.im2col_stride, pad = k / 2;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < npix;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long hwo = static_cast<long>(p.ho) * p.wo;
+    const long img = i / hwo;
+    const int rem = static_cast<int>(i - img * hwo);
+    const int oh = rem / p.wo, ow = rem - (rem / p.wo) * p.wo;
+    float v[64];
+#pragma unroll 1
+    for (int q = 0; q < p.cpad; ++q) v[q] = 0.f;
+    const long hw = static_cast<long>(p.h) * p.w;
+    for (int r = 0; r < k; ++r) {
+      const int ih = oh * st - pad + r;
+      if (ih < 0 || ih >= p.h) continue;
+      for (int s = 0; s < k; ++s) {
+        const int iw = ow * st - pad + s;
+        if (iw < 0 || iw >= p.w) continue;
+        const int base = (r * k + s) * 3;
+        if (p.format == SSN_INPUT_F32_NCHW) {
+          const float* src = static_cast<const float*>(p.raw) + img * 3 * hw +
+                             static_cast<long>(ih) * p.w + iw;
+          v[base] = __ldg(src);
+          v[base + 1] = __ldg(src + hw);
+          v[base + 2] = __ldg(src + 2 * hw);
+        } else {
+          const uint8_t* src =
+              static_cast<const uint8_t*>(p.raw) + ((img * p.h + ih) * p.w + iw) * 3;
+          v[base] = (static_cast<float>(src[0]) - 128.f) * (1.f / 64.f);
+          v[base + 1] = (static_cast<float>(src[1]) - 128.f) * (1.f / 64.f);
+          v[base + 2] = (static_cast<float>(src[2]) - 128.f) * (1.f / 64.f);
+        }
+      }
+    }
+    uint4* y = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + i * p.cpad);
+    for (int q = 0; q < p.cpad / 8; ++q) {
+      uint4 u;
+      u.x = pack_bf16x2(v[8 * q], v[8 * q + 1]);
+      u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+      u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+      u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+      y[q] = u;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // pooling, bf16 NHWC, 8 channels per thread
 
@@ -68,7 +118,7 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 }
 
 __global__ void pool_bf16_kernel(PoolParams p) {
-  const OpDesc d = load_desc(p.row, nullptr, p.op);
+  const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, G = C >> 3;
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
   __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y);
@@ -130,7 +180,7 @@ __global__ void pool_bf16_kernel(PoolParams p) {
 }
 
 __global__ void pool_f32_kernel(PoolParams p) {
-  const OpDesc d = load_desc(p.row, nullptr, p.op);
+  const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin;
   const float* x = static_cast<const float*>(p.x);
   float* y = static_cast<float*>(p.y);
@@ -178,7 +228,7 @@ __global__ void pool_f32_kernel(PoolParams p) {
 // [c_max][k_max][k_max]; centre crop to the active k.
 
 __global__ void conv_f32_kernel(ConvParams p) {
-  const OpDesc d = load_desc(p.row, p.fixed, p.op);
+  const OpDims d = load_desc(p.row, p.fixed, p.op);
   const long total = static_cast<long>(p.M) * d.cout;
   const float* x = static_cast<const float*>(p.x);
   const float* w = static_cast<const float*>(p.w);
@@ -230,7 +280,10 @@ static inline int grid_for(long work, int block) {
 }
 
 cudaError_t launch_input(const InputParams& p, cudaStream_t s) {
-  input_kernel<<<grid_for(static_cast<long>(p.n) * p.h * p.w, 256), 256, 0, s>>>(p);
+  if (p.im2col_k > 0)
+    input_im2col_kernel<<<grid_for(static_cast<long>(p.n) * p.ho * p.wo, 128), 128, 0, s>>>(p);
+  else
+    input_kernel<<<grid_for(static_cast<long>(p.n) * p.h * p.w, 256), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,9 @@ struct TensorSpec {
   int cout = 0, cin = 0, k = 1;  // max shape (depthwise: cin == 1)
   int cin_store = 0;             // stored inner dim (>= cin, multiple of 8 for bf16)
   bool depthwise = false, linear = false;
+  // stored as [cout][cin_store] over the im2col order (r*k+s)*cin+c: the
+  // stem conv whose im2col the input stage produces (bf16 OFA-ResNet50)
+  bool im2col_stem = false;
   uint32_t fan_in = 1;
   uint64_t w_off = 0, w_bytes = 0;  // blob offsets
   uint64_t b_off = 0;               // bias (linear), fp32
@@ -183,7 +186,8 @@ inline void finalize_layout(Net& net) {
   for (auto& t : net.tensors) {
     off = align(off);
     t.w_off = off;
-    t.w_bytes = uint64_t(t.cout) * t.k * t.k * t.cin_store * eb;
+    t.w_bytes = t.im2col_stem ? uint64_t(t.cout) * t.cin_store * eb
+                              : uint64_t(t.cout) * t.k * t.k * t.cin_store * eb;
     off += t.w_bytes;
   }
   for (auto& t : net.tensors) {
@@ -405,29 +409,46 @@ inline Net build_ofa_resnet50(const ssn_supernet_desc& d, const SubnetCfg* cfg) 
   const int H = static_cast<int>(d.image_size);
   const int stem_mid_a = md8(md8(64 * s.width[0]) / 2);
   const int stem_out_a = md8(64 * s.width[1]);
-  const int cin0 = bf16 ? 8 : 3;
+  const int H2 = (H + 2 - 3) / 2 + 1;
 
   // ---- segment 0: input, stem, maxpool
+  // bf16: the input stage emits the stem conv's im2col directly (3x3 s2 p1
+  // over 3 channels = 27 values, padded to 32), so stem conv0 runs as a
+  // K = 32 GEMM on the tensor cores instead of nine nearly-empty taps.
   b.begin_segment();
   b.begin_block(-1);
   {
     auto& o = b.op(OP_INPUT);
     o.in = S_RAW;
-    o.hin = o.hout = H; o.win = o.wout = H;
+    o.hin = H; o.win = H;
     o.cin_max = 3; o.cin = 3;
-    o.cout_max = o.cout = cin0;
+    if (bf16) {
+      o.k_max = o.k = 3; o.stride = 2;  // im2col geometry
+      o.hout = o.wout = H2;
+      o.cout_max = o.cout = 32;
+    } else {
+      o.hout = o.wout = H;
+      o.cout_max = o.cout = 3;
+    }
   }
   b.end_block();
-  const int H2 = (H + 2 - 3) / 2 + 1;
-  const int t0 = b.tensor(32, 3, 3, false, false, cin0);
+  const int t0 = b.tensor(32, 3, 3, false, false, bf16 ? 32 : 3);
+  if (bf16) net.tensors[t0].im2col_stem = true;
   const int n0 = b.norm(32);
   b.begin_block(-1);
   {
     auto& o = b.op(OP_CONV);
     o.tensor = t0; o.norm = n0; o.act = ACT_RELU;
-    o.k_max = o.k = 3; o.stride = 2;
-    o.hin = H; o.win = H; o.hout = H2; o.wout = H2;
-    o.cin_max = cin0; o.cin = cin0;
+    if (bf16) {
+      o.k_max = o.k = 1; o.stride = 1;
+      o.hin = o.win = H2;
+      o.cin_max = o.cin = 32;
+    } else {
+      o.k_max = o.k = 3; o.stride = 2;
+      o.hin = o.win = H;
+      o.cin_max = o.cin = 3;
+    }
+    o.hout = o.wout = H2;
     o.cout_max = 32; o.cout = stem_mid_a;
   }
   b.end_block();
