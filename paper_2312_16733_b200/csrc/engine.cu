@@ -504,12 +504,12 @@ int ssn_plan_ops(const ssn_supernet_desc* desc, const ssn_subnet_cfg* c, ssn_op_
       r.k = static_cast<uint32_t>(o.kind == OP_AVGPOOL ? o.pool_k : o.k);
       r.stride = static_cast<uint32_t>(o.stride);
       r.hin = o.hin; r.win = o.win; r.hout = o.hout; r.wout = o.wout;
+      r.cin = o.cin; r.cout = o.cout; r.cin_max = o.cin_max; r.cout_max = o.cout_max;
       if (o.tensor >= 0 && net.tensors[o.tensor].im2col_stem) {
         // report the logical convolution (3x3 s2 over 3 channels), not its GEMM form
         r.k = 3; r.stride = 2; r.cin = r.cin_max = 3;
         r.hin = r.win = net.ops[0].hin;
       }
-      r.cin = o.cin; r.cout = o.cout; r.cin_max = o.cin_max; r.cout_max = o.cout_max;
       r.depthwise = o.depthwise;
       r.block = static_cast<uint32_t>(blk[i]);
       r.segment = static_cast<uint32_t>(net.blocks[blk[i]].segment);
