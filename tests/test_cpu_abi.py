@@ -75,3 +75,23 @@ def test_ofa_encoding_to_layerselect_flags():
     c = ssn.ofa_resnet50_config([2, 0, 1, 2, 1], [0.25] * 18, [2, 1, 0, 2, 1, 0])
     assert c.depth_flags == [True, False, False, True, False, True, True, True, False]
     assert c.width_multipliers == [1.0, 0.8, 0.65, 1.0, 0.8, 0.65]
+
+
+def test_cpp_binding_against_reference_headers(tmp_path):
+    """include/ssn.hpp compiles with the unmodified servesim headers and the
+    reference's default_catalog() tuples are actuatable (host-side check)."""
+    import shutil
+    import subprocess
+    ref = "/root/reference/proj/include"
+    if not os.path.isdir(ref) or not shutil.which("g++"):
+        pytest.skip("reference headers not present")
+    exe = tmp_path / "binding"
+    inc_json = os.path.join(ROOT, "oracle", "_ref", "inc")
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT}/include", f"-I{ref}", f"-I{inc_json}",
+                    os.path.join(ROOT, "tests", "cpp", "servesim_binding.cpp"),
+                    f"-L{os.path.dirname(ssn.LIB_PATH)}", "-lssn",
+                    f"-Wl,-rpath,{os.path.dirname(ssn.LIB_PATH)}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    counts = [int(line.split()[1]) for line in out.splitlines() if line.startswith("sub")]
+    assert len(counts) == 6 and counts == sorted(counts)
+    assert "invalid_argument: width multiplier must be in (0,1]" in out
