@@ -63,10 +63,13 @@ def _cfg(cfg):
     d = (ctypes.c_uint8 * len(cfg.depth_flags))(*[1 if f else 0 for f in cfg.depth_flags])
     e = (ctypes.c_double * len(cfg.expand_ratios))(*cfg.expand_ratios)
     w = (ctypes.c_double * len(cfg.width_multipliers))(*cfg.width_multipliers)
+    ks = list(getattr(cfg, "kernel_sizes", []) or [])
+    k = (ctypes.c_uint32 * max(1, len(ks)))(*ks)
     s = _Cfg(ctypes.cast(d, ctypes.POINTER(ctypes.c_uint8)), len(d),
              ctypes.cast(e, ctypes.POINTER(ctypes.c_double)), len(e),
-             ctypes.cast(w, ctypes.POINTER(ctypes.c_double)), len(w), None, 0)
-    return s, (d, e, w)
+             ctypes.cast(w, ctypes.POINTER(ctypes.c_double)), len(w),
+             ctypes.cast(k, ctypes.POINTER(ctypes.c_uint32)) if ks else None, len(ks))
+    return s, (d, e, w, k)
 
 
 def _p(a):

@@ -260,6 +260,16 @@ static void relu_(T4* y) {
   for (size_t i = 0; i < n; ++i) y->d[i] = y->d[i] > 0.f ? y->d[i] : 0.f;
 }
 
+/* act: 1 = ReLU, 2 = h_swish(x) = x * relu6(x + 3) / 6 (OFA MyNetwork) */
+static void act_(T4* y, int act) {
+  const size_t n = t4_size(y);
+  for (size_t i = 0; i < n; ++i) {
+    const float v = y->d[i];
+    if (act == 1) y->d[i] = v > 0.f ? v : 0.f;
+    else if (act == 2) y->d[i] = v * fminf(fmaxf(v + 3.f, 0.f), 6.f) / 6.f;
+  }
+}
+
 static void add_(T4* y, const T4* r) {
   const size_t n = t4_size(y);
   for (size_t i = 0; i < n; ++i) y->d[i] += r->d[i];
@@ -278,7 +288,7 @@ static T4 conv_bn(Ctx* c, const T4* x, int tensor, int norm, int k_a, int stride
   y = conv2d(x, &c->o->t[tensor], k_a, stride, cout_a);
   subnet_norm(c, &y, &c->o->nm[norm]);
   if (res && !res_post) add_(&y, res);
-  if (relu) relu_(&y);
+  if (relu) act_(&y, relu); /* `relu` carries the activation code */
   if (res && res_post) add_(&y, res);
   store_round(c, &y);
   return y;
@@ -571,6 +581,152 @@ static void r50_forward(Ctx* c, const ssn_subnet_cfg* s, T4* x, float* logits) {
 }
 
 /* ========================================================================= */
+/* Config 3: OFA-MobileNetV3 w1.2 ([external] OFA             */
+/* OFAMobileNetV3 / DynamicMBConvLayer / DynamicSE).                           */
+/* D = 10 flags (blocks 3, 4 of each stage), E = 20, W = [1.0], K = 20.        */
+
+static const int MB_W[5] = {32, 48, 96, 136, 192};
+static const int MB_S[5] = {2, 2, 2, 1, 2};
+static const int MB_A[5] = {1, 1, 2, 2, 2};
+static const int MB_SE[5] = {0, 1, 0, 1, 1};
+
+static void mbv3_build(oracle_net* o) {
+  add_tensor(o, 24, 3, 3, 0, 0); /* first conv */
+  add_norm(o, 24, 0);
+  add_tensor(o, 24, 24, 3, 1, 0); /* first block depthwise */
+  add_norm(o, 24, 0);
+  add_tensor(o, 24, 24, 1, 0, 0); /* first block point */
+  add_norm(o, 24, 1);
+  int cin = 24;
+  for (int st = 0; st < 5; ++st)
+    for (int b = 0; b < 4; ++b) {
+      const int cout = MB_W[st], stride = b == 0 ? MB_S[st] : 1;
+      const int res = stride == 1 && cin == cout;
+      const int mid = ssn_make_divisible(ssn_round_half_even(cin * 6.0), 8);
+      add_tensor(o, mid, cin, 1, 0, 0);
+      add_norm(o, mid, 0);
+      add_tensor(o, mid, mid, 7, 1, 0);
+      add_norm(o, mid, 0);
+      if (MB_SE[st]) {
+        const int se = ssn_make_divisible(mid / 4, 8);
+        add_tensor(o, se, mid, 1, 0, 1);
+        add_tensor(o, mid, se, 1, 0, 1);
+      }
+      add_tensor(o, cout, mid, 1, 0, 0);
+      add_norm(o, cout, res);
+      cin = cout;
+    }
+  add_tensor(o, 1152, 192, 1, 0, 0);
+  add_norm(o, 1152, 0);
+  add_tensor(o, 1536, 1152, 1, 0, 0); /* feature mix: no norm, no bias */
+  add_tensor(o, o->classes, 1536, 1, 0, 1);
+}
+
+static int mbv3_check(const ssn_subnet_cfg* s) {
+  if (s->n_depth != 10 || s->n_expand != 20 || s->n_width != 1)
+    FAIL("ofa_mbv3 subnet needs 10 depth flags, 20 expand ratios, 1 width multiplier");
+  if (s->n_kernel != 0 && s->n_kernel != 20) FAIL("ofa_mbv3 subnet needs 20 kernel sizes (or none)");
+  if (s->width_multipliers[0] != 1.0)
+    FAIL("ofa_mbv3 supernet has a fixed width: width multiplier must be 1.0");
+  for (int i = 0; i < 20; ++i) {
+    if (!(s->expand_ratios[i] > 0.0) || s->expand_ratios[i] > 6.0)
+      FAIL("expand ratio must be in (0, 6]");
+    if (s->n_kernel) {
+      const uint32_t k = s->kernel_sizes[i];
+      if (k != 3 && k != 5 && k != 7) FAIL("kernel size must be 3, 5 or 7");
+    }
+  }
+  return 0;
+}
+
+/* 1x1 conv without norm (feature mix): y = act(x . W^T), bf16 storage */
+static T4 conv_act(Ctx* c, const T4* x, int tensor, int cout, int act) {
+  T4 y = conv2d(x, &c->o->t[tensor], 1, 1, cout);
+  act_(&y, act);
+  store_round(c, &y);
+  return y;
+}
+
+/* DynamicSE: x *= h_sigmoid(We[:C,:m] relu(Wr[:m,:C] mean_hw(x) + br) + be) */
+static void se_(Ctx* c, T4* x, int tr, int te) {
+  const OTensor* R = &c->o->t[tr];
+  const OTensor* E = &c->o->t[te];
+  const int C = x->c, m = ssn_make_divisible(C / 4, 8), hw = x->h * x->w;
+  float* pooled = (float*)calloc(C, sizeof(float));
+  float* hid = (float*)calloc(m, sizeof(float));
+  float* gate = (float*)calloc(C, sizeof(float));
+  for (int n = 0; n < x->n; ++n) {
+    for (int ch = 0; ch < C; ++ch) {
+      double s = 0.0;
+      for (int p = 0; p < hw; ++p) s += x->d[((size_t)n * hw + p) * C + ch];
+      pooled[ch] = (float)(s / hw);
+    }
+    for (int j = 0; j < m; ++j) {
+      float s = R->bias[j];
+      for (int ch = 0; ch < C; ++ch) s += R->w[(size_t)j * R->cin + ch] * pooled[ch];
+      hid[j] = s > 0.f ? s : 0.f;
+    }
+    for (int ch = 0; ch < C; ++ch) {
+      float s = E->bias[ch];
+      for (int j = 0; j < m; ++j) s += E->w[(size_t)ch * E->cin + j] * hid[j];
+      gate[ch] = fminf(fmaxf(s + 3.f, 0.f), 6.f) / 6.f;
+    }
+    for (int p = 0; p < hw; ++p)
+      for (int ch = 0; ch < C; ++ch) x->d[((size_t)n * hw + p) * C + ch] *= gate[ch];
+  }
+  free(pooled);
+  free(hid);
+  free(gate);
+  store_round(c, x);
+}
+
+static void mbv3_forward(Ctx* c, const ssn_subnet_cfg* s, T4* x, float* logits) {
+  T4 y = conv_bn(c, x, 0, 0, 3, 2, 24, NULL, 2, 0);
+  {
+    T4 h = conv_bn(c, &y, 1, 1, 3, 1, 24, NULL, 1, 0);
+    T4 z = conv_bn(c, &h, 2, 2, 1, 1, 24, c->count_only ? NULL : &y, 0, 0);
+    t4_free(&h);
+    t4_free(&y);
+    y = z;
+  }
+  int t = 3, nrm = 3, blk = 0, cin_max = 24;
+  for (int st = 0; st < 5; ++st)
+    for (int b = 0; b < 4; ++b, ++blk) {
+      const int cout = MB_W[st], stride = b == 0 ? MB_S[st] : 1;
+      const int res = stride == 1 && cin_max == cout;
+      const int t0 = t, n0 = nrm;
+      t += MB_SE[st] ? 5 : 3;
+      nrm += 3;
+      cin_max = cout;
+      if (b >= 2 && !s->depth_flags[2 * st + (b - 2)]) continue; /* LayerSelect */
+      const int mid = ssn_make_divisible(ssn_round_half_even(y.c * s->expand_ratios[blk]), 8);
+      const int ka = s->n_kernel ? (int)s->kernel_sizes[blk] : 7;
+      T4 h1 = conv_bn(c, &y, t0, n0, 1, 1, mid, NULL, MB_A[st], 0);
+      T4 h2 = conv_bn(c, &h1, t0 + 1, n0 + 1, ka, stride, mid, NULL, MB_A[st], 0);
+      t4_free(&h1);
+      int tp = t0 + 2;
+      if (MB_SE[st]) {
+        if (!c->count_only) se_(c, &h2, t0 + 2, t0 + 3);
+        tp = t0 + 4;
+      }
+      T4 out = conv_bn(c, &h2, tp, n0 + 2, 1, 1, cout, (res && !c->count_only) ? &y : NULL, 0, 0);
+      t4_free(&h2);
+      t4_free(&y);
+      y = out;
+    }
+  T4 f = conv_bn(c, &y, t, nrm, 1, 1, 1152, NULL, 2, 0);
+  t4_free(&y);
+  if (!c->count_only) {
+    T4 g = global_avgpool(c, &f);
+    T4 m = conv_act(c, &g, t + 1, 1536, 2);
+    linear_out(&m, &c->o->t[t + 2], logits);
+    t4_free(&g);
+    t4_free(&m);
+  }
+  t4_free(&f);
+}
+
+/* ========================================================================= */
 /* public oracle API (ctypes)                                                 */
 
 oracle_net* oracle_create(int family, uint64_t seed, int classes, int bf16_weights) {
@@ -583,6 +739,8 @@ oracle_net* oracle_create(int family, uint64_t seed, int classes, int bf16_weigh
     tinycnn_build(o);
   } else if (family == SSN_FAMILY_OFA_RESNET50) {
     r50_build(o);
+  } else if (family == SSN_FAMILY_OFA_MBV3) {
+    mbv3_build(o);
   } else {
     snprintf(g_err, sizeof g_err, "oracle: unsupported family %d", family);
     free(o);
@@ -614,12 +772,15 @@ float oracle_weight(const oracle_net* o, int tensor, int co, int ci, int r, int 
 
 static int check_cfg(const oracle_net* o, const ssn_subnet_cfg* s) {
   if (o->family == SSN_FAMILY_TINYCNN) return tinycnn_check(s);
+  if (o->family == SSN_FAMILY_OFA_MBV3) return mbv3_check(s);
   return r50_check(s);
 }
 
 static void run(Ctx* c, const ssn_subnet_cfg* s, T4* x, float* logits) {
   if (c->o->family == SSN_FAMILY_TINYCNN)
     tinycnn_forward(c, s, x, logits);
+  else if (c->o->family == SSN_FAMILY_OFA_MBV3)
+    mbv3_forward(c, s, x, logits);
   else
     r50_forward(c, s, x, logits);
 }

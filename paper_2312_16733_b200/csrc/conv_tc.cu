@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int q = 0; q < 8; ++q) o[q] += r8[q];
               }
             }
-            if (p.act == 1) {
+            if (p.act) {
 #pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
+              for (int q = 0; q < 8; ++q) o[q] = act_apply(o[q], p.act);
             }
             if (p.res && p.res_post) {
 #pragma unroll

@@ -24,6 +24,30 @@ struct alignas(64) OpDesc {
   int pad;             // k / 2
   const float* scale;  // SubnetNorm folded scale [cout] (NULL = 1)
   const float* shift;  // SubnetNorm folded shift / bias [cout] (NULL = 0)
+  int aux;             // OP_SE: active squeeze width
+};
+
+// h_swish(x) = x * relu6(x + 3) / 6 ; h_sigmoid(x) = relu6(x + 3) / 6
+__device__ __forceinline__ float act_apply(float v, int act) {
+  if (act == 1) return fmaxf(v, 0.f);
+  if (act == 2) return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
+  return v;
+}
+
+// Squeeze-excite parameters (OFA DynamicSE): weights are leading slices of
+// the max-shape reduce [se_max][c_max] / expand [c_max][se_max] tensors.
+struct SEParams {
+  void* x;                // NHWC bf16 [n][hw][C], scaled in place
+  float* pooled;          // [n][c_max] scratch
+  float* gate;            // [n][c_max] scratch
+  const void* w_reduce;   // bf16 [se_max][c_max]
+  const float* b_reduce;  // [se_max]
+  const void* w_expand;   // bf16 [c_max][se_max]
+  const float* b_expand;  // [c_max]
+  const OpDesc* const* row;
+  int op;
+  int n, hw, c_max, se_max;
+  int w_ld;  // row stride of the reduce tensor (this op's max channels)
 };
 
 // Static (graph-baked) parameters of one conv op.

@@ -40,6 +40,8 @@ cudaError_t launch_input(const InputParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
+cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s);
+cudaError_t launch_se(const SEParams& p, cudaStream_t s);
 }  // namespace ssn
 
 using namespace ssn;
@@ -117,6 +119,8 @@ struct ssn_engine {
   void* d_raw = nullptr;
   size_t raw_img_bytes = 0;
   float* d_logits = nullptr;
+  float* d_se = nullptr;  // squeeze-excite scratch: pooled + gate [max_batch][se_cmax]
+  int se_cmax = 0;
   std::vector<uint32_t> grid;
   std::map<uint64_t, std::pair<cudaGraphExec_t, int>> graphs;  // key -> (exec, kernels)
   cudaStream_t stream = nullptr;
@@ -137,7 +141,8 @@ static size_t raw_image_bytes(const ssn_supernet_desc& d) {
 
 static void validate_desc(const ssn_supernet_desc* d) {
   if (!d) SSN_THROW(SSN_E_INVALID, "null supernet descriptor");
-  if (d->family != SSN_FAMILY_TINYCNN && d->family != SSN_FAMILY_OFA_RESNET50)
+  if (d->family != SSN_FAMILY_TINYCNN && d->family != SSN_FAMILY_OFA_RESNET50 &&
+      d->family != SSN_FAMILY_OFA_MBV3)
     SSN_THROW(SSN_E_INVALID, "unsupported supernet family " + std::to_string(d->family));
   if (d->dtype != SSN_DTYPE_F32 && d->dtype != SSN_DTYPE_BF16)
     SSN_THROW(SSN_E_INVALID, "dtype must be SSN_DTYPE_F32 or SSN_DTYPE_BF16");
@@ -163,9 +168,12 @@ static void generate_blob(const Net& net, uint8_t* blob) {
             const float v = ssn_weight_value(seed, static_cast<uint32_t>(ti), idx, t.fan_in, bf16);
             // storage: KRSC [cout][k][k][cin_store] (depthwise: [c][k][k])
             // im2col stem: [cout][(r*k+s)*cin + c] padded to cin_store
+            // bf16 depthwise: tap-major [k][k][c] (16-byte channel vectors)
             const uint64_t e =
                 t.im2col_stem
                     ? static_cast<uint64_t>(o) * t.cin_store + (r * t.k + s) * t.cin + i
+                : (t.depthwise && bf16)
+                    ? static_cast<uint64_t>(r * t.k + s) * t.cout + o
                     : (static_cast<uint64_t>(o) * kk + r * t.k + s) * t.cin_store + i;
             if (bf16) {
               reinterpret_cast<uint16_t*>(blob + t.w_off)[e] = ssn_f32_to_bf16_bits(v);
@@ -274,11 +282,31 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
         if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
         CUDA_TRY(launch_conv_tc(p, wmap, s));
+      } else if (bf) {
+        CUDA_TRY(launch_dw_bf16(p, s));
       } else {
-        if (bf) SSN_THROW(SSN_E_INVALID, "bf16 depthwise conv not supported for this family");
         CUDA_TRY(launch_conv_f32(p, s));
       }
       return 1;
+    }
+    case OP_SE: {
+      SEParams p{};
+      p.x = slot_ptr(e, o.in, map);
+      p.pooled = e->d_se;
+      p.gate = e->d_se + static_cast<size_t>(e->desc.max_batch) * e->se_cmax;
+      p.w_reduce = e->d_w + e->net.tensors[o.tensor].w_off;
+      p.b_reduce = reinterpret_cast<const float*>(e->d_w + e->net.tensors[o.tensor].b_off);
+      p.w_expand = e->d_w + e->net.tensors[o.tensor2].w_off;
+      p.b_expand = reinterpret_cast<const float*>(e->d_w + e->net.tensors[o.tensor2].b_off);
+      p.row = e->d_rowptr;
+      p.op = oi;
+      p.n = static_cast<int>(batch);
+      p.hw = o.hout * o.wout;
+      p.c_max = e->se_cmax;
+      p.se_max = o.se_mid_max;
+      p.w_ld = o.cin_max;
+      CUDA_TRY(launch_se(p, s));
+      return 3;
     }
   }
   SSN_THROW(SSN_E_INVALID, "unknown op kind");
@@ -434,6 +462,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     }
     if (o.kind == OP_LINEAR)
       dsc.shift = reinterpret_cast<const float*>(e->d_w + e->net.tensors[o.tensor].b_off);
+    if (o.kind == OP_SE) dsc.aux = o.se_mid;
   }
   CUDA_TRY(cudaMalloc(&st.d_row, row.size() * sizeof(OpDesc)));
   CUDA_TRY(cudaMemcpy(st.d_row, row.data(), row.size() * sizeof(OpDesc), cudaMemcpyHostToDevice));
@@ -565,6 +594,10 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     CUDA_TRY(cudaMalloc(&e->d_raw, e->raw_img_bytes * desc->max_batch));
     CUDA_TRY(cudaMemset(e->d_raw, 0, e->raw_img_bytes * desc->max_batch));
     CUDA_TRY(cudaMalloc(&e->d_logits, static_cast<size_t>(desc->max_batch) * desc->num_classes * 4));
+    for (const OpSpec& o : e->net.ops)
+      if (o.kind == OP_SE) e->se_cmax = std::max(e->se_cmax, o.cin_max);
+    if (e->se_cmax)
+      CUDA_TRY(cudaMalloc(&e->d_se, 2ull * desc->max_batch * e->se_cmax * sizeof(float)));
     CUDA_TRY(cudaMalloc(&e->d_rowptr, sizeof(OpDesc*)));
     CUDA_TRY(cudaMemset(e->d_rowptr, 0, sizeof(OpDesc*)));
     CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
@@ -585,6 +618,7 @@ void ssn_destroy(ssn_engine* e) {
   for (int i = 0; i < NBUF; ++i) cudaFree(e->bufs[i]);
   cudaFree(e->d_raw);
   cudaFree(e->d_logits);
+  cudaFree(e->d_se);
   cudaFree(e->d_rowptr);
   cudaFree(e->d_w);
   if (e->stream) cudaStreamDestroy(e->stream);

@@ -261,9 +261,145 @@ __global__ void conv_f32_kernel(ConvParams p) {
     float v = acc * (d.scale ? d.scale[co] : 1.f) + (d.shift ? d.shift[co] : 0.f);
     const float* res = static_cast<const float*>(p.res);
     if (res && !p.res_post) v += res[m * d.cout + co];
-    if (p.act == 1) v = fmaxf(v, 0.f);
+    v = act_apply(v, p.act);
     if (res && p.res_post) v += res[m * d.cout + co];
     static_cast<float*>(p.y)[m * d.cout + co] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bf16 depthwise k x k conv (OFA elastic kernel: centre crop of k_max) fused
+// with SubnetNorm + activation.  Weights tap-major [k_max*k_max][c_max] so a
+// thread's 8 channels of one tap are one 16-byte load; 8 channels per thread,
+// consecutive threads walk channels of one pixel (coalesced NHWC).
+
+__global__ void dw_bf16_kernel(ConvParams p) {
+  const OpDims d = load_desc(p.row, p.fixed, p.op);
+  const int C = d.cout, G = C >> 3;
+  const int k = d.k, pad = d.pad, off = (p.k_max - k) / 2;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
+  const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w);
+  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y);
+  const long total = static_cast<long>(p.M) * G;
+  const int hwo = p.ho * p.wo;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long m = i / G;
+    const int g = static_cast<int>(i - m * G);
+    const int img = static_cast<int>(m / hwo);
+    const int rem = static_cast<int>(m - static_cast<long>(img) * hwo);
+    const int oh = rem / p.wo, ow = rem - (rem / p.wo) * p.wo;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = 0; r < k; ++r) {
+      const int ih = oh * p.stride - pad + r;
+      if (ih < 0 || ih >= p.h) continue;
+      for (int s = 0; s < k; ++s) {
+        const int iw = ow * p.stride - pad + s;
+        if (iw < 0 || iw >= p.w_) continue;
+        float xv[8], wv[8];
+        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(
+                          x + (static_cast<long>(img * p.h + ih) * p.w_ + iw) * C + g * 8)),
+                      xv);
+        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(
+                          w + static_cast<long>((r + off) * p.k_max + (s + off)) * p.cout_max +
+                          g * 8)),
+                      wv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += xv[q] * wv[q];
+      }
+    }
+    float o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = g * 8 + q;
+      o[q] = act_apply(acc[q] * (d.scale ? d.scale[c] : 1.f) + (d.shift ? d.shift[c] : 0.f),
+                       p.act);
+    }
+    *reinterpret_cast<uint4*>(y + m * C + g * 8) = f32_to_bf16x8(o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Squeeze-excite (OFA DynamicSE): pool -> reduce FC + ReLU -> expand FC +
+// h_sigmoid -> scale the activation in place.
+
+// pooled[n][c] = mean over hw; grid (n, ceil(C/64)), 256 threads:
+// 8 channel groups x 32 pixel lanes, shared-memory reduction over lanes.
+__global__ void se_pool_kernel(SEParams p) {
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin;
+  const int n = blockIdx.x, c0 = blockIdx.y * 64;
+  if (c0 >= C) return;
+  const int g = threadIdx.x & 7, lane = threadIdx.x >> 3;
+  const int c = c0 + g * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * p.hw * C;
+  if (c < C) {
+    for (int q = lane; q < p.hw; q += 32) {
+      float f[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * C + c)), f);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] += f[t];
+    }
+  }
+  __shared__ float red[32][65];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) red[lane][g * 8 + t] = acc[t];
+  __syncthreads();
+  if (threadIdx.x < 64 && c0 + threadIdx.x < C) {
+    float s = 0.f;
+    for (int l = 0; l < 32; ++l) s += red[l][threadIdx.x];
+    p.pooled[static_cast<long>(n) * p.c_max + c0 + threadIdx.x] = s / static_cast<float>(p.hw);
+  }
+}
+
+// gate[n][c] = h_sigmoid(We[c, :mid] . relu(Wr[:mid, :C] . pooled[n] + br) + be[c])
+__global__ void se_fc_kernel(SEParams p) {
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const OpDesc* dp = desc_ptr(p.row, nullptr, p.op);
+  const int C = d.cin, mid = dp->aux;
+  const int n = blockIdx.x;
+  extern __shared__ float sh[];
+  float* pin = sh;          // [C]
+  float* hid = sh + p.c_max;  // [mid]
+  const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.w_reduce);
+  const __nv_bfloat16* we = static_cast<const __nv_bfloat16*>(p.w_expand);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) pin[c] = p.pooled[static_cast<long>(n) * p.c_max + c];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < mid; j += nw) {  // one warp per hidden unit, coalesced row read
+    float s = 0.f;
+    for (int c = lane; c < C; c += 32)
+      s += __bfloat162float(wr[static_cast<long>(j) * p.w_ld + c]) * pin[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) hid[j] = fmaxf(s + p.b_reduce[j], 0.f);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s = p.b_expand[c];
+    for (int j = 0; j < mid; ++j) s += __bfloat162float(we[static_cast<long>(c) * p.se_max + j]) * hid[j];
+    p.gate[static_cast<long>(n) * p.c_max + c] = fminf(fmaxf(s + 3.f, 0.f), 6.f) * (1.f / 6.f);
+  }
+}
+
+__global__ void se_scale_kernel(SEParams p) {
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin, G = C >> 3;
+  __nv_bfloat16* x = static_cast<__nv_bfloat16*>(p.x);
+  const long total = static_cast<long>(p.n) * p.hw * G;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long pix = i / G;
+    const int g = static_cast<int>(i - pix * G);
+    const int n = static_cast<int>(pix / p.hw);
+    uint4* ptr = reinterpret_cast<uint4*>(x + pix * C + g * 8);
+    float f[8];
+    bf16x8_to_f32(*ptr, f);
+    const float* gt = p.gate + static_cast<long>(n) * p.c_max + g * 8;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) f[t] *= gt[t];
+    *ptr = f32_to_bf16x8(f);
   }
 }
 
@@ -301,6 +437,18 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
 
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s) {
   conv_f32_kernel<<<grid_for(static_cast<long>(p.M) * p.cout_max, 128), 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
+  dw_bf16_kernel<<<grid_for(static_cast<long>(p.M) * (p.cout_max / 8), 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
+  se_pool_kernel<<<dim3(p.n, (p.c_max + 63) / 64), 256, 0, s>>>(p);
+  se_fc_kernel<<<p.n, 256, (p.c_max + p.se_max) * sizeof(float), s>>>(p);
+  se_scale_kernel<<<grid_for(static_cast<long>(p.n) * p.hw * (p.c_max / 8), 256), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

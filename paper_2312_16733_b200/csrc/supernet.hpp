@@ -29,6 +29,7 @@ enum OpKind : int {
   OP_AVGPOOL = 3,  // k = s, ceil_mode
   OP_GAP = 4,      // global average pool -> [N][C]
   OP_LINEAR = 5,   // classifier (fp32 logits)
+  OP_SE = 6,       // squeeze-excite: x *= h_sigmoid(W2 relu(W1 gap(x) + b1) + b2)
 };
 
 // Logical buffer slots inside a block; mapped to arena buffers per graph.
@@ -43,7 +44,7 @@ enum Slot : int {
   S_LOGITS = 6,  // fp32 logits
 };
 
-enum Act : int { ACT_NONE = 0, ACT_RELU = 1 };
+enum Act : int { ACT_NONE = 0, ACT_RELU = 1, ACT_HSWISH = 2 };
 
 struct TensorSpec {
   int cout = 0, cin = 0, k = 1;  // max shape (depthwise: cin == 1)
@@ -68,6 +69,8 @@ struct OpSpec {
   int in = S_IN, out = S_OUT, res = S_NONE;
   bool res_post = false;  // residual added after the activation
   int tensor = -1, norm = -1;
+  int tensor2 = -1;            // OP_SE: expand tensor (tensor = reduce)
+  int se_mid = 0, se_mid_max = 0;
   int act = ACT_NONE;
   int stride = 1, k_max = 1, pool_k = 0;
   int hin = 0, win = 0, hout = 0, wout = 0;
@@ -597,10 +600,217 @@ inline Net build_ofa_resnet50(const ssn_supernet_desc& d, const SubnetCfg* cfg) 
   return net;
 }
 
+// ---------------------------------------------------------------------------
+// Config 3 — OFA-MobileNetV3, width 1.2 ([external] OFA
+// OFAMobileNetV3 / DynamicMBConvLayer / DynamicSE).  D = 10 flags (blocks 3-4
+// of each of the 5 stages), E = 20 per-block expand ratios (<= 6), K = 20
+// per-block depthwise kernel sizes (3/5/7, centre crop of 7x7), W = [1.0]
+// (the supernet's width is fixed).
+
+inline Net build_ofa_mbv3(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
+  static const int WIDTH[5] = {32, 48, 96, 136, 192};  // md(24/40/80/112/160 * 1.2)
+  static const int STRIDE[5] = {2, 2, 2, 1, 2};
+  static const int ACT[5] = {ACT_RELU, ACT_RELU, ACT_HSWISH, ACT_HSWISH, ACT_HSWISH};
+  static const bool SE[5] = {false, true, false, true, true};
+  static const double MAX_E = 6.0;
+  SubnetCfg mx;
+  mx.depth.assign(10, 1);
+  mx.expand.assign(20, MAX_E);
+  mx.width.assign(1, 1.0);
+  mx.kernel.assign(20, 7);
+  const SubnetCfg& s = cfg ? *cfg : mx;
+  if (s.depth.size() != 10 || s.expand.size() != 20 || s.width.size() != 1)
+    throw std::invalid_argument(
+        "ofa_mbv3 subnet needs 10 depth flags, 20 expand ratios, 1 width multiplier");
+  if (!s.kernel.empty() && s.kernel.size() != 20)
+    throw std::invalid_argument("ofa_mbv3 subnet needs 20 kernel sizes (or none)");
+  if (s.width[0] != 1.0)
+    throw std::invalid_argument("ofa_mbv3 supernet has a fixed width: width multiplier must be 1.0");
+  for (double e : s.expand)
+    if (!(e > 0.0) || e > MAX_E) throw std::invalid_argument("expand ratio must be in (0, 6]");
+  for (uint32_t k : s.kernel)
+    if (k != 3 && k != 5 && k != 7) throw std::invalid_argument("kernel size must be 3, 5 or 7");
+
+  Net net;
+  net.desc = d;
+  if (d.dtype != SSN_DTYPE_BF16) throw std::invalid_argument("ofa_mbv3 runs in bf16");
+  net.elem_bytes = 2;
+  Builder b(net);
+  const int H = static_cast<int>(d.image_size);
+  const int H2 = (H + 2 - 3) / 2 + 1;
+
+  // ---- segment 0: input (stem im2col), first conv, first block
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_INPUT);
+    o.in = S_RAW;
+    o.hin = o.win = H;
+    o.k_max = o.k = 3; o.stride = 2;
+    o.hout = o.wout = H2;
+    o.cin_max = o.cin = 3;
+    o.cout_max = o.cout = 32;
+  }
+  b.end_block();
+  const int t0 = b.tensor(24, 3, 3, false, false, 32);
+  net.tensors[t0].im2col_stem = true;
+  const int n0 = b.norm(24);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);
+    o.tensor = t0; o.norm = n0; o.act = ACT_HSWISH;
+    o.k_max = o.k = 1;
+    o.hin = o.win = o.hout = o.wout = H2;
+    o.cin_max = o.cin = 32;
+    o.cout_max = o.cout = 24;
+  }
+  b.end_block();
+  // first block: MBConv(expand 1): dw 3x3 + BN + ReLU, point 1x1 + BN, identity residual
+  const int t1 = b.tensor(24, 1, 3, true, false);
+  const int n1 = b.norm(24);
+  const int t2 = b.tensor(24, 24, 1, false, false);
+  const int n2 = b.norm(24, true);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);
+    o.in = S_IN; o.out = S_T1;
+    o.tensor = t1; o.norm = n1; o.act = ACT_RELU; o.depthwise = true;
+    o.k_max = o.k = 3;
+    o.hin = o.win = o.hout = o.wout = H2;
+    o.cin_max = o.cin = o.cout_max = o.cout = 24;
+  }
+  {
+    auto& o = b.op(OP_CONV);
+    o.in = S_T1; o.out = S_OUT; o.res = S_IN;
+    o.tensor = t2; o.norm = n2; o.act = ACT_NONE;
+    o.hin = o.win = o.hout = o.wout = H2;
+    o.cin_max = o.cin = o.cout_max = o.cout = 24;
+  }
+  b.end_block();
+
+  // ---- segments 1..5: inverted-residual stages
+  int hw = H2, cin_max = 24, cin_a = 24, blk = 0;
+  for (int st = 0; st < 5; ++st) {
+    b.begin_segment();
+    for (int bi = 0; bi < 4; ++bi, ++blk) {
+      const int flag = bi >= 2 ? 2 * st + (bi - 2) : -1;
+      const int stride = bi == 0 ? STRIDE[st] : 1;
+      const int cout = WIDTH[st];
+      const bool res = stride == 1 && cin_max == cout;
+      const int mid_max = md8(rnd(cin_max * MAX_E));
+      const int mid = md8(rnd(cin_a * s.expand[blk]));
+      const int ka = s.kernel.empty() ? 7 : static_cast<int>(s.kernel[blk]);
+      const int hw_out = (hw - 1) / stride + 1;  // "same" padding k/2
+      const int ti = b.tensor(mid_max, cin_max, 1, false, false);
+      const int ni = b.norm(mid_max);
+      const int td = b.tensor(mid_max, 1, 7, true, false);
+      const int nd = b.norm(mid_max);
+      int tr = -1, te = -1;
+      const int se_max = md8(mid_max / 4);
+      if (SE[st]) {
+        tr = b.tensor(se_max, mid_max, 1, false, true);  // reduce (+bias)
+        te = b.tensor(mid_max, se_max, 1, false, true);  // expand (+bias)
+      }
+      const int tp = b.tensor(cout, mid_max, 1, false, false);
+      const int np = b.norm(cout, res);
+      b.begin_block(flag);
+      {
+        auto& o = b.op(OP_CONV);
+        o.in = S_IN; o.out = S_T1;
+        o.tensor = ti; o.norm = ni; o.act = ACT[st];
+        o.hin = o.win = o.hout = o.wout = hw;
+        o.cin_max = cin_max; o.cin = cin_a;
+        o.cout_max = mid_max; o.cout = mid;
+      }
+      {
+        auto& o = b.op(OP_CONV);
+        o.in = S_T1; o.out = S_T2;
+        o.tensor = td; o.norm = nd; o.act = ACT[st]; o.depthwise = true;
+        o.k_max = 7; o.k = ka; o.stride = stride;
+        o.hin = o.win = hw; o.hout = o.wout = hw_out;
+        o.cin_max = o.cout_max = mid_max;
+        o.cin = o.cout = mid;
+      }
+      if (SE[st]) {
+        auto& o = b.op(OP_SE);
+        o.in = S_T2; o.out = S_T2;  // scales in place
+        o.tensor = tr; o.tensor2 = te;
+        o.hin = o.win = o.hout = o.wout = hw_out;
+        o.cin_max = o.cout_max = mid_max;
+        o.cin = o.cout = mid;
+        o.se_mid = md8(mid / 4);
+        o.se_mid_max = se_max;
+      }
+      {
+        auto& o = b.op(OP_CONV);
+        o.in = S_T2; o.out = S_OUT;
+        o.res = res ? S_IN : S_NONE;
+        o.tensor = tp; o.norm = np; o.act = ACT_NONE;
+        o.hin = o.win = o.hout = o.wout = hw_out;
+        o.cin_max = mid_max; o.cin = mid;
+        o.cout_max = o.cout = cout;
+      }
+      b.end_block();
+      const bool on = flag < 0 || s.depth[flag];
+      if (on) cin_a = cout;
+      cin_max = cout;
+      hw = hw_out;
+    }
+  }
+
+  // ---- segment 6: final expand, pool, feature mix, classifier
+  b.begin_segment();
+  const int tf = b.tensor(1152, 192, 1, false, false);
+  const int nf = b.norm(1152);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);
+    o.tensor = tf; o.norm = nf; o.act = ACT_HSWISH;
+    o.hin = o.win = o.hout = o.wout = hw;
+    o.cin_max = o.cin = 192;
+    o.cout_max = o.cout = 1152;
+  }
+  b.end_block();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_GAP);
+    o.hin = o.win = hw;
+    o.hout = o.wout = 1;
+    o.cin_max = o.cout_max = o.cin = o.cout = 1152;
+  }
+  b.end_block();
+  const int tm = b.tensor(1536, 1152, 1, false, false);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_CONV);  // feature mix: no norm, no bias
+    o.tensor = tm; o.act = ACT_HSWISH;
+    o.hin = o.win = o.hout = o.wout = 1;
+    o.cin_max = o.cin = 1152;
+    o.cout_max = o.cout = 1536;
+  }
+  b.end_block();
+  const int tl = b.tensor(static_cast<int>(d.num_classes), 1536, 1, false, true);
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_LINEAR);
+    o.out = S_LOGITS;
+    o.tensor = tl;
+    o.hin = o.win = o.hout = o.wout = 1;
+    o.cin_max = o.cin = 1536;
+    o.cout_max = o.cout = static_cast<int>(d.num_classes);
+  }
+  b.end_block();
+  finalize_layout(net);
+  mark_blocks(net, s.depth);
+  assign_stats(net);
+  return net;
+}
+
 inline Net build_net(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
   switch (d.family) {
     case SSN_FAMILY_TINYCNN: return build_tinycnn(d, cfg);
     case SSN_FAMILY_OFA_RESNET50: return build_ofa_resnet50(d, cfg);
+    case SSN_FAMILY_OFA_MBV3: return build_ofa_mbv3(d, cfg);
     default: throw std::invalid_argument("unsupported supernet family");
   }
 }

@@ -92,7 +92,7 @@ def ofa_resnet50_preset(name: str) -> SubnetConfig:
 # ---------------------------------------------------------------------------
 # plan accounting (algorithmic FLOPs / bytes per image)
 
-OP_KINDS = {0: "input", 1: "conv", 2: "maxpool", 3: "avgpool", 4: "gap", 5: "linear"}
+OP_KINDS = {0: "input", 1: "conv", 2: "maxpool", 3: "avgpool", 4: "gap", 5: "linear", 6: "se"}
 
 
 def plan_ops(desc, cfg: SubnetConfig):
@@ -144,6 +144,8 @@ def plan_cost(desc, cfg: SubnetConfig, elem_bytes: int = 2):
                 b = hw_in * r["cin"] * elem_bytes + r["cout"] * 4
         elif kind == "input":
             b = hw_in * 3 * 4 + hw_out * r["cout"] * elem_bytes
+        elif kind == "se":  # pool read + scale read/write of the activation
+            b = 3 * hw_in * r["cin"] * elem_bytes
         else:
             b = (hw_in * r["cin"] + hw_out * r["cout"]) * elem_bytes
         flops += f

@@ -207,6 +207,72 @@ def resnet50(seed):
     return forward, net
 
 
+def hswish(x):
+    return x * torch.clamp(x + 3, 0, 6) / 6
+
+
+def mbv3(seed):
+    """OFA-MobileNetV3 w1.2 (DynamicMBConvLayer, DynamicSE), bf16-valued weights."""
+    net = Net(seed, bf16=True)
+    W, S, A, SE = [32, 48, 96, 136, 192], [2, 2, 2, 1, 2], [1, 1, 2, 2, 2], [0, 1, 0, 1, 1]
+    first = (net.tensor((24, 3, 3, 3)), net.norm(24))
+    fb = (net.tensor((24, 1, 3, 3)), net.norm(24), net.tensor((24, 24, 1, 1)), net.norm(24, True))
+    cin, blocks = 24, []
+    for st in range(5):
+        for b in range(4):
+            cout, stride = W[st], (S[st] if b == 0 else 1)
+            res = stride == 1 and cin == cout
+            mid = md8(round(cin * 6.0))
+            ib = (net.tensor((mid, cin, 1, 1)), net.norm(mid))
+            dw = (net.tensor((mid, 1, 7, 7)), net.norm(mid))
+            se = None
+            if SE[st]:
+                sm = md8(mid // 4)
+                se = (net.tensor((sm, mid, 1, 1), linear=True), net.tensor((mid, sm, 1, 1), linear=True))
+            pl = (net.tensor((cout, mid, 1, 1)), net.norm(cout, res))
+            blocks.append((st, b, stride, res, ib, dw, se, pl))
+            cin = cout
+    fe = (net.tensor((1152, 192, 1, 1)), net.norm(1152))
+    fm = net.tensor((1536, 1152, 1, 1))
+    net.tensor((1000, 1536, 1, 1), linear=True)  # classifier (weights last in net.w)
+    fc = len(net.w) - 1
+
+    def act(y, a):
+        return torch.relu(y) if a == 1 else hswish(y)
+
+    def forward(run, cfg, x):
+        D, E, Wl, K = cfg
+        biases = list(net.bias)  # linear tensors in ordinal order: SE pairs, then classifier
+        y = act(run.conv_bn(x, *first, 3, 2, 24, relu=False), 2)
+        h = run.conv_bn(y, fb[0], fb[1], 3, 1, 24, groups=24)
+        y = run.conv_bn(h, fb[2], fb[3], 1, 1, 24, res=y, relu=False)
+        se_i = 0
+        for idx, (st, b, stride, res, ib, dw, se, pl) in enumerate(blocks):
+            if se is not None:
+                se_biases = (biases[se_i], biases[se_i + 1])
+                se_i += 2
+            if b >= 2 and not D[2 * st + b - 2]:
+                continue
+            mid = md8(round(y.shape[1] * E[idx]))
+            h = act(run.conv_bn(y, ib[0], ib[1], 1, 1, mid, relu=False), A[st])
+            h = act(run.conv_bn(h, dw[0], dw[1], K[idx], stride, mid, groups=mid, relu=False), A[st])
+            if se is not None:
+                C = h.shape[1]
+                m = md8(C // 4)
+                wr = net.w[se[0]][:m, :C, 0, 0]
+                we = net.w[se[1]][:C, :m, 0, 0]
+                p = h.mean(dim=(2, 3))
+                s1 = torch.relu(p @ wr.T + se_biases[0][:m])
+                s2 = torch.clamp(s1 @ we.T + se_biases[1][:C] + 3, 0, 6) / 6
+                h = h * s2[:, :, None, None]
+            y = run.conv_bn(h, pl[0], pl[1], 1, 1, W[st], res=y if res else None, relu=False)
+        y = hswish(run.conv_bn(y, *fe, 1, 1, 1152, relu=False))
+        g = y.mean(dim=(2, 3))
+        f = hswish(g @ net.w[fm][:, :, 0, 0].T)
+        return f @ net.w[fc][:, :, 0, 0].T + biases[-1]
+    return forward, net
+
+
 def calibrate_and_forward(fwd, netobj, cfg, cal_x, x):
     r = Run(netobj, True)
     fwd(r, cfg, torch.from_numpy(cal_x))
@@ -243,6 +309,18 @@ def main():
         m, v, lg = calibrate_and_forward(fwd, netobj, cfg, cal_x, x)
         out[f"r50_{name}_mean"], out[f"r50_{name}_var"], out[f"r50_{name}_logits"] = m, v, lg
     out["r50_cfgs"] = np.array(repr(r50_cfgs))
+    # ---- OFA-MobileNetV3 w1.2 (config 3) at 64x64
+    mb_cfgs = {
+        "min": ([False] * 10, [3.0] * 20, [1.0], [3] * 20),
+        "max": ([True] * 10, [6.0] * 20, [1.0], [7] * 20),
+        "mixed": ([True, False] * 5, [3.0, 4.0, 6.0, 4.0] * 5, [1.0], [3, 5, 7, 5] * 5),
+    }
+    fwd, netobj = mbv3(seed)
+    cal_x, x = images(seed, 100, 8, 64), images(seed, 1, 4, 64)
+    for name, cfg in mb_cfgs.items():
+        m, v, lg = calibrate_and_forward(fwd, netobj, cfg, cal_x, x)
+        out[f"mb_{name}_mean"], out[f"mb_{name}_var"], out[f"mb_{name}_logits"] = m, v, lg
+    out["mb_cfgs"] = np.array(repr(mb_cfgs))
     # ---- operator fixtures: WeightSlice conv with slices, crop, depthwise
     rng = np.random.default_rng(0)
     ops = []

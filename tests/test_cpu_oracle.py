@@ -155,3 +155,36 @@ def test_oracle_bf16_storage_emulation_is_close(r50_oracle):
     a = r50_oracle.forward(cfg, x, mean=m, var=v)
     b = r50_oracle.forward(cfg, x, mean=m, var=v, bf16_storage=True)
     assert rel(b, a) < 2e-2
+
+
+MB = {k: ssn.SubnetConfig(*map(list, v)) for k, v in ast.literal_eval(str(GOLD["mb_cfgs"])).items()}
+
+
+@pytest.fixture(scope="module")
+def mb_oracle():
+    return O.OracleNet(ssn.FAMILY_OFA_MBV3, seed=0, classes=1000, bf16_weights=True)
+
+
+@pytest.mark.parametrize("name", list(MB))
+def test_oracle_mbv3_matches_torch(mb_oracle, name):
+    cfg = MB[name]
+    m, v = mb_oracle.calibrate(cfg, O.images(0, 100, 8, 64))
+    assert rel(m, GOLD[f"mb_{name}_mean"]) < 1e-4
+    assert rel(v, GOLD[f"mb_{name}_var"]) < 1e-4
+    lg = mb_oracle.forward(cfg, O.images(0, 1, 4, 64), mean=m, var=v)
+    assert rel(lg, GOLD[f"mb_{name}_logits"]) < 1e-4
+
+
+def test_mbv3_survey_numbers(mb_oracle):
+    """SURVEY §8 a11/config 3: MBv3-max 25,416 SubnetNorm channels;
+    0.385 / 1.679 GFLOP per image (min d2 e3 k3 / max d4 e6 k7)."""
+    d = ssn.make_desc(ssn.FAMILY_OFA_MBV3)
+    lo, hi = MB["min"], MB["max"]
+    assert ssn.plan_stat_count(d, hi) == 25416 == mb_oracle.stat_count(hi)
+    assert ssn.plan_stat_count(d, lo) == mb_oracle.stat_count(lo)
+    assert abs(ssn.plan_cost(d, lo)["flops"] / 1e9 - 0.385) < 0.005
+    assert abs(ssn.plan_cost(d, hi)["flops"] / 1e9 - 1.679) < 0.005
+    with pytest.raises(ValueError, match="kernel size must be 3, 5 or 7"):
+        ssn.plan_stat_count(d, ssn.SubnetConfig([True] * 10, [3.0] * 20, [1.0], [4] * 20))
+    with pytest.raises(ValueError, match="fixed width"):
+        ssn.plan_stat_count(d, ssn.SubnetConfig([True] * 10, [3.0] * 20, [0.5], [3] * 20))

@@ -188,3 +188,42 @@ def test_actuation_moves_no_weights(r50):
     st = eng.stats()
     assert st["weight_bytes"] == before["weight_bytes"] == ssn.weight_blob_bytes(desc)
     assert st["last_actuate_us"] < 1000.0
+
+
+# ---------------------------------------------------------------- config 3
+MB_CASES = {
+    "min": ssn.SubnetConfig([False] * 10, [3.0] * 20, [1.0], [3] * 20),
+    "max": ssn.SubnetConfig([True] * 10, [6.0] * 20, [1.0], [7] * 20),
+    "mixed": ssn.SubnetConfig([True, False] * 5, [3.0, 4.0, 6.0, 4.0] * 5, [1.0], [3, 5, 7, 5] * 5),
+}
+
+
+@pytest.fixture(scope="module")
+def mbv3(gpu):
+    desc = ssn.make_desc(ssn.FAMILY_OFA_MBV3, ssn.DTYPE_BF16, image_size=224, num_classes=1000,
+                         max_batch=8, seed=SEED)
+    eng = ssn.Engine(desc)
+    on = O.OracleNet(ssn.FAMILY_OFA_MBV3, seed=SEED, classes=1000, bf16_weights=True)
+    eng.prepare([4, 8])
+    yield eng, on
+    eng.close()
+
+
+@pytest.mark.parametrize("name", list(MB_CASES))
+def test_ofa_mbv3_bf16_parity(mbv3, name):
+    """Config 3: depthwise k in {3,5,7} (centre crop), SE, h_swish, 224x224."""
+    eng, on = mbv3
+    cfg = MB_CASES[name]
+    sid = list(MB_CASES).index(name)
+    m, v = on.calibrate(cfg, O.images(SEED, 100, 8, 224))
+    eng.register_subnet(sid, cfg, m, v)
+    x = O.images(SEED, 5, 8, 224)
+    eng.actuate(sid)
+    got = eng.infer(x, 8, 8)
+    emu = on.forward(cfg, x, mean=m, var=v, bf16_storage=True)
+    ref = on.forward(cfg, x, mean=m, var=v)
+    e_emu, e_ref = rel(got, emu), rel(got, ref)
+    print(f"mbv3 {name}: rel vs bf16-storage oracle {e_emu:.2e}, vs fp32 oracle {e_ref:.2e}")
+    assert e_emu <= 2e-2
+    assert e_ref <= 2e-2
+    argmax_agree(got, ref, tol=4 * e_ref * np.abs(ref).max())
