@@ -238,9 +238,12 @@ class Engine:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib_handle is not None:
-            _lib_handle.ssn_destroy(h)
-        self._h = ctypes.c_void_p()
+        try:
+            if h is not None and h.value and _lib_handle is not None:
+                _lib_handle.ssn_destroy(h)
+            self._h = None
+        except Exception:  # interpreter shutdown: module globals already torn down
+            pass
 
     __del__ = close
 

@@ -306,7 +306,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.se_max = o.se_mid_max;
       p.w_ld = o.cin_max;
       CUDA_TRY(launch_se(p, s));
-      return 3;
+      return 4;
     }
   }
   SSN_THROW(SSN_E_INVALID, "unknown op kind");
@@ -594,10 +594,15 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     CUDA_TRY(cudaMalloc(&e->d_raw, e->raw_img_bytes * desc->max_batch));
     CUDA_TRY(cudaMemset(e->d_raw, 0, e->raw_img_bytes * desc->max_batch));
     CUDA_TRY(cudaMalloc(&e->d_logits, static_cast<size_t>(desc->max_batch) * desc->num_classes * 4));
+    int se_hmax = 0;
     for (const OpSpec& o : e->net.ops)
-      if (o.kind == OP_SE) e->se_cmax = std::max(e->se_cmax, o.cin_max);
-    if (e->se_cmax)
-      CUDA_TRY(cudaMalloc(&e->d_se, 2ull * desc->max_batch * e->se_cmax * sizeof(float)));
+      if (o.kind == OP_SE) {
+        e->se_cmax = std::max(e->se_cmax, o.cin_max);
+        se_hmax = std::max(se_hmax, o.se_mid_max);
+      }
+    if (e->se_cmax)  // pooled [B][cmax] | gate [B][cmax] | hidden [B][hmax]
+      CUDA_TRY(cudaMalloc(&e->d_se, 1ull * desc->max_batch * (2 * e->se_cmax + se_hmax) *
+                                        sizeof(float)));
     CUDA_TRY(cudaMalloc(&e->d_rowptr, sizeof(OpDesc*)));
     CUDA_TRY(cudaMemset(e->d_rowptr, 0, sizeof(OpDesc*)));
     CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));

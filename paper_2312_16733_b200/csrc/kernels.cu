@@ -270,52 +270,94 @@ __global__ void conv_f32_kernel(ConvParams p) {
 // ---------------------------------------------------------------------------
 // bf16 depthwise k x k conv (OFA elastic kernel: centre crop of k_max) fused
 // with SubnetNorm + activation.  Weights tap-major [k_max*k_max][c_max] so a
-// thread's 8 channels of one tap are one 16-byte load; 8 channels per thread,
-// consecutive threads walk channels of one pixel (coalesced NHWC).
+// thread's 8 channels of one tap are one 16-byte load.  Each thread computes
+// DW_Q horizontally adjacent outputs of one 8-channel group: per kernel row
+// it loads the (DW_Q-1)*stride + k input pixels and k weights ONCE and reuses
+// them from registers (k=7: 17 loads per row instead of 98 per 4 outputs).
+// Consecutive threads walk channel groups of one pixel quad (coalesced NHWC).
 
-__global__ void dw_bf16_kernel(ConvParams p) {
+constexpr int DW_Q = 4;  // adjacent outputs per thread
+constexpr int DW_C = 4;  // channels per thread (8-byte vectors keep registers low)
+
+__device__ __forceinline__ void bf16x4_to_f32(const uint2& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+
+template <int STRIDE>
+__global__ void __launch_bounds__(256) dw_bf16_kernel(ConvParams p) {
+  constexpr int DW_SEG = (DW_Q - 1) * STRIDE + 7;  // input pixels per row for k_max = 7
   const OpDims d = load_desc(p.row, p.fixed, p.op);
-  const int C = d.cout, G = C >> 3;
+  const int C = d.cout, G = C / DW_C;
   const int k = d.k, pad = d.pad, off = (p.k_max - k) / 2;
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
   const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w);
   __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y);
-  const long total = static_cast<long>(p.M) * G;
-  const int hwo = p.ho * p.wo;
+  const int wq = (p.wo + DW_Q - 1) / DW_Q;
+  const long total = static_cast<long>(p.n) * p.ho * wq * G;
+  const int nseg = (DW_Q - 1) * STRIDE + k;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const long m = i / G;
-    const int g = static_cast<int>(i - m * G);
-    const int img = static_cast<int>(m / hwo);
-    const int rem = static_cast<int>(m - static_cast<long>(img) * hwo);
-    const int oh = rem / p.wo, ow = rem - (rem / p.wo) * p.wo;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = 0; r < k; ++r) {
-      const int ih = oh * p.stride - pad + r;
-      if (ih < 0 || ih >= p.h) continue;
-      for (int s = 0; s < k; ++s) {
-        const int iw = ow * p.stride - pad + s;
-        if (iw < 0 || iw >= p.w_) continue;
-        float xv[8], wv[8];
-        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(
-                          x + (static_cast<long>(img * p.h + ih) * p.w_ + iw) * C + g * 8)),
-                      xv);
-        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(
-                          w + static_cast<long>((r + off) * p.k_max + (s + off)) * p.cout_max +
-                          g * 8)),
-                      wv);
+    const int g = static_cast<int>(i % G);
+    long rest = i / G;
+    const int qx = static_cast<int>(rest % wq);
+    rest /= wq;
+    const int oh = static_cast<int>(rest % p.ho);
+    const int img = static_cast<int>(rest / p.ho);
+    const int ow0 = qx * DW_Q;
+    const int iw0 = ow0 * STRIDE - pad;
+    float acc[DW_Q][DW_C];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] += xv[q] * wv[q];
+    for (int q = 0; q < DW_Q; ++q)
+#pragma unroll
+      for (int c = 0; c < DW_C; ++c) acc[q][c] = 0.f;
+    for (int r = 0; r < k; ++r) {
+      const int ih = oh * STRIDE - pad + r;
+      if (ih < 0 || ih >= p.h) continue;
+      const __nv_bfloat16* xrow = x + (static_cast<long>(img * p.h + ih) * p.w_) * C + g * DW_C;
+      float seg[DW_SEG][DW_C];
+#pragma unroll
+      for (int t = 0; t < DW_SEG; ++t) {
+        const int iw = iw0 + t;
+        if (t < nseg && iw >= 0 && iw < p.w_) {
+          bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(xrow + static_cast<long>(iw) * C)), seg[t]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < DW_C; ++c) seg[t][c] = 0.f;
+        }
+      }
+      const __nv_bfloat16* wrow =
+          w + static_cast<long>((r + off) * p.k_max + off) * p.cout_max + g * DW_C;
+#pragma unroll
+      for (int s = 0; s < 7; ++s) {
+        if (s >= k) break;
+        float wv[DW_C];
+        bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(wrow + static_cast<long>(s) * p.cout_max)), wv);
+#pragma unroll
+        for (int q = 0; q < DW_Q; ++q)
+#pragma unroll
+          for (int c = 0; c < DW_C; ++c) acc[q][c] += seg[q * STRIDE + s][c] * wv[c];
       }
     }
-    float o[8];
+    float sc[DW_C], sh[DW_C];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = g * 8 + q;
-      o[q] = act_apply(acc[q] * (d.scale ? d.scale[c] : 1.f) + (d.shift ? d.shift[c] : 0.f),
-                       p.act);
+    for (int c = 0; c < DW_C; ++c) {
+      sc[c] = d.scale ? d.scale[g * DW_C + c] : 1.f;
+      sh[c] = d.shift ? d.shift[g * DW_C + c] : 0.f;
     }
-    *reinterpret_cast<uint4*>(y + m * C + g * 8) = f32_to_bf16x8(o);
+#pragma unroll
+    for (int q = 0; q < DW_Q; ++q) {
+      const int ow = ow0 + q;
+      if (ow >= p.wo) break;
+      float o[DW_C];
+#pragma unroll
+      for (int c = 0; c < DW_C; ++c) o[c] = act_apply(acc[q][c] * sc[c] + sh[c], p.act);
+      uint2 pk;
+      pk.x = pack_bf16x2(o[0], o[1]);
+      pk.y = pack_bf16x2(o[2], o[3]);
+      *reinterpret_cast<uint2*>(y + (static_cast<long>(img * p.ho + oh) * p.wo + ow) * C + g * DW_C) = pk;
+    }
   }
 }
 
@@ -353,33 +395,68 @@ __global__ void se_pool_kernel(SEParams p) {
   }
 }
 
-// gate[n][c] = h_sigmoid(We[c, :mid] . relu(Wr[:mid, :C] . pooled[n] + br) + be[c])
-__global__ void se_fc_kernel(SEParams p) {
+// gate[n][c] = h_sigmoid(We[c, :mid] . relu(Wr[:mid, :C] . pooled[n] + br) + be[c]),
+// as two kernels gridded over (SE_NB-sample batch, output rows) so the weight
+// rows are read once per SE_NB samples and every SM has work.  hid lives in
+// the tail of the gate scratch (fp32 [n][se_max]).
+constexpr int SE_NB = 8;
+constexpr int SE_ROWS = 32;  // output rows per block (8 warps x 4)
+
+__device__ __forceinline__ float* se_hid(const SEParams& p) {
+  return p.gate + static_cast<long>(p.n) * p.c_max;
+}
+
+__global__ void se_reduce_kernel(SEParams p) {
   const OpDims d = load_desc(p.row, nullptr, p.op);
-  const OpDesc* dp = desc_ptr(p.row, nullptr, p.op);
-  const int C = d.cin, mid = dp->aux;
-  const int n = blockIdx.x;
-  extern __shared__ float sh[];
-  float* pin = sh;          // [C]
-  float* hid = sh + p.c_max;  // [mid]
+  const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
+  const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.w_reduce);
-  const __nv_bfloat16* we = static_cast<const __nv_bfloat16*>(p.w_expand);
-  for (int c = threadIdx.x; c < C; c += blockDim.x) pin[c] = p.pooled[static_cast<long>(n) * p.c_max + c];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < mid; j += nw) {  // one warp per hidden unit, coalesced row read
-    float s = 0.f;
-    for (int c = lane; c < C; c += 32)
-      s += __bfloat162float(wr[static_cast<long>(j) * p.w_ld + c]) * pin[c];
+  float* hid = se_hid(p);
+  for (int j = blockIdx.y * SE_ROWS + warp; j < min(mid, (blockIdx.y + 1) * SE_ROWS); j += 8) {
+    float acc[SE_NB];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) hid[j] = fmaxf(s + p.b_reduce[j], 0.f);
+    for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
+    for (int c = lane; c < C; c += 32) {
+      const float wv = __bfloat162float(wr[static_cast<long>(j) * p.w_ld + c]);
+#pragma unroll
+      for (int b = 0; b < SE_NB; ++b)
+        if (b < nb) acc[b] += wv * p.pooled[static_cast<long>(n0 + b) * p.c_max + c];
+    }
+#pragma unroll
+    for (int b = 0; b < SE_NB; ++b) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+      if (lane == 0 && b < nb) hid[static_cast<long>(n0 + b) * p.se_max + j] = fmaxf(acc[b] + p.b_reduce[j], 0.f);
+    }
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = p.b_expand[c];
-    for (int j = 0; j < mid; ++j) s += __bfloat162float(we[static_cast<long>(c) * p.se_max + j]) * hid[j];
-    p.gate[static_cast<long>(n) * p.c_max + c] = fminf(fmaxf(s + 3.f, 0.f), 6.f) * (1.f / 6.f);
+}
+
+__global__ void se_expand_kernel(SEParams p) {
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
+  const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const __nv_bfloat16* we = static_cast<const __nv_bfloat16*>(p.w_expand);
+  const float* hid = se_hid(p);
+  for (int c = blockIdx.y * SE_ROWS + warp; c < min(C, (blockIdx.y + 1) * SE_ROWS); c += 8) {
+    float acc[SE_NB];
+#pragma unroll
+    for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
+    for (int j = lane; j < mid; j += 32) {
+      const float wv = __bfloat162float(we[static_cast<long>(c) * p.se_max + j]);
+#pragma unroll
+      for (int b = 0; b < SE_NB; ++b)
+        if (b < nb) acc[b] += wv * hid[static_cast<long>(n0 + b) * p.se_max + j];
+    }
+#pragma unroll
+    for (int b = 0; b < SE_NB; ++b) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+      if (lane == 0 && b < nb)
+        p.gate[static_cast<long>(n0 + b) * p.c_max + c] =
+            fminf(fmaxf(acc[b] + p.b_expand[c] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+    }
   }
 }
 
@@ -441,13 +518,19 @@ cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
-  dw_bf16_kernel<<<grid_for(static_cast<long>(p.M) * (p.cout_max / 8), 256), 256, 0, s>>>(p);
+  const long work = static_cast<long>(p.n) * p.ho * ((p.wo + DW_Q - 1) / DW_Q) * (p.cout_max / DW_C);
+  if (p.stride == 2)
+    dw_bf16_kernel<2><<<grid_for(work, 256), 256, 0, s>>>(p);
+  else
+    dw_bf16_kernel<1><<<grid_for(work, 256), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
   se_pool_kernel<<<dim3(p.n, (p.c_max + 63) / 64), 256, 0, s>>>(p);
-  se_fc_kernel<<<p.n, 256, (p.c_max + p.se_max) * sizeof(float), s>>>(p);
+  const int nbk = (p.n + SE_NB - 1) / SE_NB;
+  se_reduce_kernel<<<dim3(nbk, (p.se_max + SE_ROWS - 1) / SE_ROWS), 256, 0, s>>>(p);
+  se_expand_kernel<<<dim3(nbk, (p.c_max + SE_ROWS - 1) / SE_ROWS), 256, 0, s>>>(p);
   se_scale_kernel<<<grid_for(static_cast<long>(p.n) * p.hw * (p.c_max / 8), 256), 256, 0, s>>>(p);
   return cudaGetLastError();
 }

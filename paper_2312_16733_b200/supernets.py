@@ -155,3 +155,24 @@ def plan_cost(desc, cfg: SubnetConfig, elem_bytes: int = 2):
         row.update(op=kind, flops=f, bytes=b, weight_bytes=wb)
         per.append(row)
     return dict(flops=flops, act_bytes=act_bytes, weight_bytes=w_bytes, per_op=per)
+
+
+def ofa_mbv3_config(d: Sequence[int], e: Sequence[float], k: Sequence[int]) -> SubnetConfig:
+    """OFA-MBv3 (d[5] in {2,3,4}, e[20], ks[20]) -> engine SubnetConfig."""
+    d = list(d) if len(d) == 5 else [d[0]] * 5
+    flags = []
+    for s in range(5):
+        flags += [d[s] >= 3, d[s] >= 4]
+    e = list(e) if len(e) == 20 else [e[0]] * 20
+    k = list(k) if len(k) == 20 else [k[0]] * 20
+    return SubnetConfig(flags, [float(x) for x in e], [1.0], [int(x) for x in k])
+
+
+def ofa_mbv3_preset(name: str) -> SubnetConfig:
+    """min (d2 e3 k3) / mid (d3 e4 k5) / max (d4 e6 k7) of SURVEY.md §8(d) config 3."""
+    d, e, k = {"min": (2, 3.0, 3), "mid": (3, 4.0, 5), "max": (4, 6.0, 7)}[name]
+    return ofa_mbv3_config([d] * 5, [e] * 20, [k] * 20)
+
+
+def preset(family: int, name: str) -> SubnetConfig:
+    return ofa_mbv3_preset(name) if family == 3 else ofa_resnet50_preset(name)

@@ -21,6 +21,7 @@ ap.add_argument("--subnets", default="min,mid,max")
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--image", type=int, default=224)
 ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--family", default="r50", choices=["r50", "mbv3"])
 ap.add_argument("--json", default="")
 a = ap.parse_args()
 
@@ -41,11 +42,12 @@ for r in rows:
             continue
         launches.append((name, float(d["Metric Value"].replace(",", "")) / 1e3))
 
-desc = ssn.make_desc(ssn.FAMILY_OFA_RESNET50, image_size=a.image, max_batch=a.batch)
+fam = ssn.FAMILY_OFA_MBV3 if a.family == "mbv3" else ssn.FAMILY_OFA_RESNET50
+desc = ssn.make_desc(fam, image_size=a.image, max_batch=a.batch)
 names = a.subnets.split(",")
 per_fwd = []
 for n in names:
-    cost = ssn.plan_cost(desc, ssn.ofa_resnet50_preset(n))
+    cost = ssn.plan_cost(desc, ssn.supernets.preset(fam, n))
     per_fwd.append((n, [p for p in cost["per_op"] if p is not None]))
 # the last len(names) forwards in the list are the measured step
 need = sum(len(ops) for _, ops in per_fwd)

@@ -15,13 +15,15 @@ ap.add_argument("--image", type=int, default=224)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--subnets", default="min,mid,max")
+ap.add_argument("--family", default="r50", choices=["r50", "mbv3"])
 a = ap.parse_args()
 names = a.subnets.split(",")
-desc = ssn.make_desc(ssn.FAMILY_OFA_RESNET50, ssn.DTYPE_BF16, image_size=a.image,
+fam = ssn.FAMILY_OFA_MBV3 if a.family == "mbv3" else ssn.FAMILY_OFA_RESNET50
+desc = ssn.make_desc(fam, ssn.DTYPE_BF16, image_size=a.image,
                      num_classes=1000, max_batch=a.batch, input_format=ssn.INPUT_U8_NHWC)
 eng = ssn.Engine(desc)
 for i, n in enumerate(names):
-    eng.register_subnet(i, ssn.ofa_resnet50_preset(n))
+    eng.register_subnet(i, ssn.supernets.preset(fam, n))
 eng.prepare([a.batch])
 x = torch.randint(0, 256, (a.batch, a.image, a.image, 3), dtype=torch.uint8, device="cuda")
 for it in range(a.warmup + a.steps):
