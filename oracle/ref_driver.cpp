@@ -78,8 +78,10 @@ int main(int argc, char** argv) try {
       out << r.start_us << '\t' << r.completion_us << '\t' << r.worker << '\t'
           << r.subnet_index << '\t' << r.actual_count << '\t'
           << r.profiled_batch << '\t' << r.predicted_latency_us << '\t'
-          << r.actuation_us << '\t' << (r.query_ids.empty() ? 0 : r.query_ids.front())
-          << '\n';
+          << r.actuation_us << '\t' << r.batch_deadline_us << '\t';
+      for (std::size_t i = 0; i < r.query_ids.size(); ++i)
+        out << (i ? "," : "") << r.query_ids[i];
+      out << '\n';
     }
     std::cout << report_to_json(rep).dump() << '\n';
     return 0;
