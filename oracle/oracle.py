@@ -52,6 +52,9 @@ def lib():
         L.oracle_num_tensors.argtypes = [P]
         L.oracle_set_threads.argtypes = [i32]
         L.oracle_images.argtypes = [u64, u32, i32, i32, P]
+        L.oracle_forward_tokens.restype = i32
+        L.oracle_forward_tokens.argtypes = [P, cp, P, i32, i32, i32, P]
+        L.oracle_tokens.argtypes = [u64, u32, i32, i32, P]
         L.oracle_conv_op.restype = i32
         L.oracle_conv_op.argtypes = [P, i32, i32, i32, i32, P, i32, i32, i32, i32, i32, i32,
                                      i32, i32, P, P, P, i32, P]
@@ -116,6 +119,17 @@ class OracleNet:
             raise ValueError(lib().oracle_last_error().decode())
         return out
 
+    def forward_tokens(self, cfg, ids, bf16_storage=False):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        n, seq = ids.shape
+        out = np.zeros((n, self.classes), dtype=np.float32)
+        s, keep = _cfg(cfg)
+        rc = lib().oracle_forward_tokens(self.h, ctypes.byref(s), _p(ids), n, seq,
+                                         1 if bf16_storage else 0, _p(out))
+        if rc:
+            raise ValueError(lib().oracle_last_error().decode())
+        return out
+
     def calibrate(self, cfg, x_nchw):
         """SubnetNorm calibration: per-subnet (mu, var) from batch statistics."""
         x = np.ascontiguousarray(x_nchw, dtype=np.float32)
@@ -134,6 +148,12 @@ class OracleNet:
 def images(seed: int, batch_ordinal: int, n: int, hw: int) -> np.ndarray:
     out = np.zeros((n, 3, hw, hw), np.float32)
     lib().oracle_images(seed, batch_ordinal, n, hw, out.ctypes.data)
+    return out
+
+
+def tokens(seed: int, batch_ordinal: int, n: int, seq: int) -> np.ndarray:
+    out = np.zeros((n, seq), np.int32)
+    lib().oracle_tokens(seed, batch_ordinal, n, seq, out.ctypes.data)
     return out
 
 

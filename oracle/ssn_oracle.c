@@ -727,6 +727,169 @@ static void mbv3_forward(Ctx* c, const ssn_subnet_cfg* s, T4* x, float* logits) 
 }
 
 /* ========================================================================= */
+/* Config 5: width/depth-sliced BERT-base-like encoder (DESIGN.md §3.4,       */
+/* [external] DynaBERT).  D = 12 layer flags, E = [FFN width], W = [heads].   */
+
+#define BT_HID 768
+#define BT_FFN 3072
+#define BT_L 12
+#define BT_VOCAB 30522
+
+static void bert_build(oracle_net* o) {
+  add_tensor(o, BT_VOCAB, BT_HID, 1, 0, 0); /* token embeddings */
+  add_tensor(o, 512, BT_HID, 1, 0, 0);      /* positions */
+  add_tensor(o, 2, BT_HID, 1, 0, 0);        /* token types */
+  add_norm(o, BT_HID, 0);
+  for (int l = 0; l < BT_L; ++l) {
+    for (int q = 0; q < 4; ++q) add_tensor(o, BT_HID, BT_HID, 1, 0, 1); /* Q K V O */
+    add_norm(o, BT_HID, 0);
+    add_tensor(o, BT_FFN, BT_HID, 1, 0, 1);
+    add_tensor(o, BT_HID, BT_FFN, 1, 0, 1);
+    add_norm(o, BT_HID, 0);
+  }
+  add_tensor(o, BT_HID, BT_HID, 1, 0, 1);       /* pooler */
+  add_tensor(o, o->classes, BT_HID, 1, 0, 1);   /* classifier */
+}
+
+static int bert_check(const ssn_subnet_cfg* s) {
+  if (s->n_depth != BT_L || s->n_expand != 1 || s->n_width != 1)
+    FAIL("bert subnet needs 12 depth flags, 1 FFN width (expand) ratio, 1 head width multiplier");
+  if (!(s->width_multipliers[0] > 0.0) || s->width_multipliers[0] > 1.0)
+    FAIL("width multiplier must be in (0,1]");
+  if (!(s->expand_ratios[0] > 0.0) || s->expand_ratios[0] > 1.0)
+    FAIL("FFN expand ratio must be in (0,1]");
+  return 0;
+}
+
+/* y[t][:cout] = x[t][:cin] . W[:cout][:cin]^T + b[:cout] (+ act), rows x cols */
+static float* linear_(const float* x, int rows, int cin, const OTensor* T, int cout, int act) {
+  float* y = (float*)malloc(sizeof(float) * (size_t)rows * cout);
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < rows; ++r)
+    for (int co = 0; co < cout; ++co) {
+      const float* wp = T->w + (size_t)co * T->cin;
+      const float* xp = x + (size_t)r * cin;
+      float acc = 0.f;
+#pragma omp simd reduction(+ : acc)
+      for (int i = 0; i < cin; ++i) acc += xp[i] * wp[i];
+      float v = acc + T->bias[co];
+      if (act == 3) v = 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+      if (act == 4) v = tanhf(v);
+      y[(size_t)r * cout + co] = v;
+    }
+  return y;
+}
+
+static void round_buf(Ctx* c, float* v, size_t n) {
+  if (!c->emulate_bf16) return;
+  for (size_t i = 0; i < n; ++i) v[i] = ssn_round_bf16(v[i]);
+}
+
+/* LayerNorm (eps 1e-12, BERT) over rows of BT_HID, in place */
+static void layernorm_(float* x, int rows, const ONorm* N) {
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < rows; ++r) {
+    float* v = x + (size_t)r * BT_HID;
+    double m = 0.0, q = 0.0;
+    for (int i = 0; i < BT_HID; ++i) m += v[i];
+    m /= BT_HID;
+    for (int i = 0; i < BT_HID; ++i) q += (v[i] - m) * (v[i] - m);
+    const float inv = 1.f / sqrtf((float)(q / BT_HID) + 1e-12f);
+    for (int i = 0; i < BT_HID; ++i) v[i] = (float)((v[i] - m) * inv) * N->gamma[i] + N->beta[i];
+  }
+}
+
+static void bert_forward(Ctx* c, const ssn_subnet_cfg* s, const int* ids, int n, int S,
+                         float* logits) {
+  const oracle_net* o = c->o;
+  const int heads = ssn_round_half_even(12 * s->width_multipliers[0]) < 1
+                        ? 1
+                        : ssn_round_half_even(12 * s->width_multipliers[0]);
+  int ffn = ssn_make_divisible(BT_FFN * s->expand_ratios[0], 8);
+  if (ffn > BT_FFN) ffn = BT_FFN;
+  const int Ca = heads * 64, T = n * S;
+  float* X = (float*)malloc(sizeof(float) * (size_t)T * BT_HID);
+  for (int t = 0; t < T; ++t) {
+    int id = ids[t];
+    if (id < 0) id = 0;
+    if (id >= BT_VOCAB) id = BT_VOCAB - 1;
+    for (int i = 0; i < BT_HID; ++i)
+      X[(size_t)t * BT_HID + i] = o->t[0].w[(size_t)id * BT_HID + i] +
+                                  o->t[1].w[(size_t)(t % S) * BT_HID + i] + o->t[2].w[i];
+  }
+  layernorm_(X, T, &o->nm[0]);
+  round_buf(c, X, (size_t)T * BT_HID);
+  for (int l = 0; l < BT_L; ++l) {
+    if (!s->depth_flags[l]) continue; /* LayerSelect */
+    const int tb = 3 + 6 * l;
+    float* Q = linear_(X, T, BT_HID, &o->t[tb], Ca, 0);
+    float* K = linear_(X, T, BT_HID, &o->t[tb + 1], Ca, 0);
+    float* V = linear_(X, T, BT_HID, &o->t[tb + 2], Ca, 0);
+    round_buf(c, Q, (size_t)T * Ca);
+    round_buf(c, K, (size_t)T * Ca);
+    round_buf(c, V, (size_t)T * Ca);
+    float* ctx = (float*)calloc((size_t)T * Ca, sizeof(float));
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int b = 0; b < n; ++b)
+      for (int h = 0; h < heads; ++h) {
+        float* sc = (float*)malloc(sizeof(float) * S);
+        for (int i = 0; i < S; ++i) {
+          const float* qi = Q + ((size_t)b * S + i) * Ca + h * 64;
+          float mx = -INFINITY;
+          for (int j = 0; j < S; ++j) {
+            const float* kj = K + ((size_t)b * S + j) * Ca + h * 64;
+            float d = 0.f;
+            for (int e = 0; e < 64; ++e) d += qi[e] * kj[e];
+            sc[j] = d * 0.125f;
+            mx = sc[j] > mx ? sc[j] : mx;
+          }
+          double sum = 0.0;
+          for (int j = 0; j < S; ++j) {
+            sc[j] = expf(sc[j] - mx);
+            sum += sc[j];
+          }
+          float* out = ctx + ((size_t)b * S + i) * Ca + h * 64;
+          for (int j = 0; j < S; ++j) {
+            const float pj = (float)(sc[j] / sum);
+            const float* vj = V + ((size_t)b * S + j) * Ca + h * 64;
+            for (int e = 0; e < 64; ++e) out[e] += pj * vj[e];
+          }
+        }
+        free(sc);
+      }
+    round_buf(c, ctx, (size_t)T * Ca);
+    float* O = linear_(ctx, T, Ca, &o->t[tb + 3], BT_HID, 0);
+    for (size_t i = 0; i < (size_t)T * BT_HID; ++i) O[i] += X[i];
+    round_buf(c, O, (size_t)T * BT_HID);
+    layernorm_(O, T, &o->nm[1 + 2 * l]);
+    round_buf(c, O, (size_t)T * BT_HID);
+    float* F = linear_(O, T, BT_HID, &o->t[tb + 4], ffn, 3);
+    round_buf(c, F, (size_t)T * ffn);
+    float* Y = linear_(F, T, ffn, &o->t[tb + 5], BT_HID, 0);
+    for (size_t i = 0; i < (size_t)T * BT_HID; ++i) Y[i] += O[i];
+    round_buf(c, Y, (size_t)T * BT_HID);
+    layernorm_(Y, T, &o->nm[2 + 2 * l]);
+    round_buf(c, Y, (size_t)T * BT_HID);
+    free(Q); free(K); free(V); free(ctx); free(O); free(F); free(X);
+    X = Y;
+  }
+  float* cls = (float*)malloc(sizeof(float) * (size_t)n * BT_HID);
+  for (int b = 0; b < n; ++b)
+    memcpy(cls + (size_t)b * BT_HID, X + (size_t)b * S * BT_HID, sizeof(float) * BT_HID);
+  float* P = linear_(cls, n, BT_HID, &o->t[3 + 6 * BT_L], BT_HID, 4);
+  round_buf(c, P, (size_t)n * BT_HID);
+  float* L = linear_(P, n, BT_HID, &o->t[4 + 6 * BT_L], o->classes, 0);
+  memcpy(logits, L, sizeof(float) * (size_t)n * o->classes);
+  free(cls); free(P); free(L); free(X);
+}
+
+/* Synthetic token ids (ssn_rng.h kind 8): floor(u01 * vocab). */
+void oracle_tokens(uint64_t seed, uint32_t batch_ordinal, int n, int s, int* out) {
+  for (long i = 0; i < (long)n * s; ++i)
+    out[i] = (int)(ssn_u01(seed, ssn_stream(SSN_STREAM_TOKENS, batch_ordinal), i) * BT_VOCAB);
+}
+
+/* ========================================================================= */
 /* public oracle API (ctypes)                                                 */
 
 oracle_net* oracle_create(int family, uint64_t seed, int classes, int bf16_weights) {
@@ -741,6 +904,8 @@ oracle_net* oracle_create(int family, uint64_t seed, int classes, int bf16_weigh
     r50_build(o);
   } else if (family == SSN_FAMILY_OFA_MBV3) {
     mbv3_build(o);
+  } else if (family == SSN_FAMILY_BERT) {
+    bert_build(o);
   } else {
     snprintf(g_err, sizeof g_err, "oracle: unsupported family %d", family);
     free(o);
@@ -773,6 +938,7 @@ float oracle_weight(const oracle_net* o, int tensor, int co, int ci, int r, int 
 static int check_cfg(const oracle_net* o, const ssn_subnet_cfg* s) {
   if (o->family == SSN_FAMILY_TINYCNN) return tinycnn_check(s);
   if (o->family == SSN_FAMILY_OFA_MBV3) return mbv3_check(s);
+  if (o->family == SSN_FAMILY_BERT) return bert_check(s);
   return r50_check(s);
 }
 
@@ -787,6 +953,7 @@ static void run(Ctx* c, const ssn_subnet_cfg* s, T4* x, float* logits) {
 
 long oracle_stat_count(oracle_net* o, const ssn_subnet_cfg* s) {
   if (check_cfg(o, s)) return -1;
+  if (o->family == SSN_FAMILY_BERT) return 0; /* LayerNorm keeps no statistics */
   Ctx c;
   memset(&c, 0, sizeof c);
   c.o = o;
@@ -885,5 +1052,18 @@ int oracle_conv_op(const float* x, int n, int h, int w, int cin, const float* wg
       y[(size_t)p * cout + co] = v;
     }
   }
+  return 0;
+}
+
+/* BERT forward on token ids [n][s] (flags bit0: bf16 storage emulation) */
+int oracle_forward_tokens(oracle_net* o, const ssn_subnet_cfg* s, const int* ids, int n, int seq,
+                          int flags, float* logits) {
+  if (o->family != SSN_FAMILY_BERT) FAIL("oracle_forward_tokens: not a transformer supernet");
+  if (check_cfg(o, s)) return -1;
+  Ctx c;
+  memset(&c, 0, sizeof c);
+  c.o = o;
+  c.emulate_bf16 = flags & 1;
+  bert_forward(&c, s, ids, n, seq, logits);
   return 0;
 }

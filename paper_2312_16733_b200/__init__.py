@@ -25,6 +25,7 @@ from .supernets import (  # noqa: F401  (re-exported)
     default_catalog_configs,
     ofa_resnet50_config,
     ofa_resnet50_preset,
+    bert_config,
     plan_cost,
     plan_ops,
     tinycnn_config,

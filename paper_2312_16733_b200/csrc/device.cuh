@@ -31,8 +31,46 @@ struct alignas(64) OpDesc {
 __device__ __forceinline__ float act_apply(float v, int act) {
   if (act == 1) return fmaxf(v, 0.f);
   if (act == 2) return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
+  if (act == 3) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));  // GELU (erf)
+  if (act == 4) return tanhf(v);
   return v;
 }
+
+// Transformer ops (config 5): token embedding + LayerNorm, attention, LayerNorm
+struct EmbedParams {
+  const int* ids;        // [n][s] token ids
+  const void* tok;       // bf16 [vocab][hid]
+  const void* pos;       // bf16 [512][hid]
+  const void* typ;       // bf16 [2][hid]
+  const float* gamma;
+  const float* beta;
+  void* y;               // bf16 [n*s][hid]
+  int n, s, hid, vocab;
+};
+
+struct LnParams {
+  const void* x;  // bf16 [rows][hid]
+  void* y;
+  const float* gamma;
+  const float* beta;
+  int rows, hid;
+};
+
+struct AttnParams {
+  const void* q;  // bf16 [n*s][c], c = heads_a * 64 (active)
+  const void* k;
+  const void* v;
+  void* o;
+  const OpDesc* const* row;
+  int op;
+  int n, s;
+};
+
+struct Token0Params {
+  const void* x;  // bf16 [n][s][c]
+  void* y;        // bf16 [n][c]
+  int n, s, c;
+};
 
 // Squeeze-excite parameters (OFA DynamicSE): weights are leading slices of
 // the max-shape reduce [se_max][c_max] / expand [c_max][se_max] tensors.

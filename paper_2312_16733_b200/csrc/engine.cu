@@ -42,6 +42,10 @@ cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
 cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_se(const SEParams& p, cudaStream_t s);
+cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s);
+cudaError_t launch_layernorm(const LnParams& p, cudaStream_t s);
+cudaError_t launch_token0(const Token0Params& p, cudaStream_t s);
+cudaError_t launch_attention(const AttnParams& p, int max_heads, cudaStream_t s);
 }  // namespace ssn
 
 using namespace ssn;
@@ -90,8 +94,8 @@ static int guarded(F&& f) {
 // ---------------------------------------------------------------------------
 // engine
 
-static constexpr int NBUF = 6;  // BND0, BND1, P, T1, T2, T3
-enum { B_BND0 = 0, B_BND1 = 1, B_P = 2, B_T1 = 3, B_T2 = 4, B_T3 = 5 };
+static constexpr int NBUF = 8;  // BND0, BND1, P, T1..T5
+enum { B_BND0 = 0, B_BND1 = 1, B_P = 2, B_T1 = 3, B_T2 = 4, B_T3 = 5, B_T4 = 6, B_T5 = 7 };
 
 struct SubnetState {
   bool ok = false;
@@ -136,13 +140,14 @@ static uint64_t graph_key(int seg, uint32_t mask, uint32_t batch) {
 
 static size_t raw_image_bytes(const ssn_supernet_desc& d) {
   const size_t px = static_cast<size_t>(d.image_size) * d.image_size;
+  if (d.family == SSN_FAMILY_BERT) return static_cast<size_t>(d.image_size) * 4;  // int32 ids
   return d.input_format == SSN_INPUT_U8_NHWC ? px * 3 : px * 3 * 4;
 }
 
 static void validate_desc(const ssn_supernet_desc* d) {
   if (!d) SSN_THROW(SSN_E_INVALID, "null supernet descriptor");
   if (d->family != SSN_FAMILY_TINYCNN && d->family != SSN_FAMILY_OFA_RESNET50 &&
-      d->family != SSN_FAMILY_OFA_MBV3)
+      d->family != SSN_FAMILY_OFA_MBV3 && d->family != SSN_FAMILY_BERT)
     SSN_THROW(SSN_E_INVALID, "unsupported supernet family " + std::to_string(d->family));
   if (d->dtype != SSN_DTYPE_F32 && d->dtype != SSN_DTYPE_BF16)
     SSN_THROW(SSN_E_INVALID, "dtype must be SSN_DTYPE_F32 or SSN_DTYPE_BF16");
@@ -289,6 +294,56 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       }
       return 1;
     }
+    case OP_EMBED: {
+      EmbedParams p{};
+      p.ids = static_cast<const int*>(e->d_raw);
+      p.tok = e->d_w + e->net.tensors[o.tensor].w_off;
+      p.pos = e->d_w + e->net.tensors[o.tensor2].w_off;
+      p.typ = e->d_w + e->net.tensors[o.tensor3].w_off;
+      p.gamma = reinterpret_cast<const float*>(e->d_w + e->net.norms[o.norm].gamma_off);
+      p.beta = reinterpret_cast<const float*>(e->d_w + e->net.norms[o.norm].beta_off);
+      p.y = slot_ptr(e, o.out, map);
+      p.n = static_cast<int>(batch);
+      p.s = o.hin;
+      p.hid = o.cout_max;
+      p.vocab = e->net.tensors[o.tensor].cout;
+      CUDA_TRY(launch_embed(p, s));
+      return 1;
+    }
+    case OP_LAYERNORM: {
+      LnParams p{};
+      p.x = slot_ptr(e, o.in, map);
+      p.y = slot_ptr(e, o.out, map);
+      p.gamma = reinterpret_cast<const float*>(e->d_w + e->net.norms[o.norm].gamma_off);
+      p.beta = reinterpret_cast<const float*>(e->d_w + e->net.norms[o.norm].beta_off);
+      p.rows = static_cast<int>(batch) * o.hin * o.win;
+      p.hid = o.cout_max;
+      CUDA_TRY(launch_layernorm(p, s));
+      return 1;
+    }
+    case OP_TOKEN0: {
+      Token0Params p{};
+      p.x = slot_ptr(e, o.in, map);
+      p.y = slot_ptr(e, o.out, map);
+      p.n = static_cast<int>(batch);
+      p.s = o.hin;
+      p.c = o.cout_max;
+      CUDA_TRY(launch_token0(p, s));
+      return 1;
+    }
+    case OP_ATTN: {
+      AttnParams p{};
+      p.q = slot_ptr(e, o.in, map);
+      p.k = slot_ptr(e, o.in2, map);
+      p.v = slot_ptr(e, o.in3, map);
+      p.o = slot_ptr(e, o.out, map);
+      p.row = e->d_rowptr;
+      p.op = oi;
+      p.n = static_cast<int>(batch);
+      p.s = o.hin;
+      CUDA_TRY(launch_attention(p, o.cin_max / o.k_max, s));
+      return 1;
+    }
     case OP_SE: {
       SEParams p{};
       p.x = slot_ptr(e, o.in, map);
@@ -317,7 +372,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
 // the next segment's boundary buffer.  `hook(op, before)` brackets each op.
 struct SlotMap {
   int op;
-  int map[5];
+  int map[9];
 };
 
 // The ops one LayerSelect variant of a segment runs, each with its slot ->
@@ -348,6 +403,8 @@ static std::vector<SlotMap> segment_plan(const ssn_engine* e, int seg, uint32_t 
     sm.map[S_T1] = B_T1;
     sm.map[S_T2] = B_T2;
     sm.map[S_T3] = B_T3;
+    sm.map[S_T4] = B_T4;
+    sm.map[S_T5] = B_T5;
     const BlockSpec& b = e->net.blocks[act[i]];
     for (int q = 0; q < b.count; ++q) {
       sm.op = b.first + q;
@@ -403,7 +460,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
   std::vector<int64_t> norm_off(plan.ops.size(), -1);
   for (size_t oi = 0; oi < plan.ops.size(); ++oi) {
     const OpSpec& o = plan.ops[oi];
-    if (!o.active || o.norm < 0) continue;
+    if (!has_subnet_norm(o)) continue;
     norm_off[oi] = static_cast<int64_t>(norm.size());
     const auto& g = e->gamma[o.norm];
     const auto& b = e->beta[o.norm];
@@ -460,7 +517,8 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
       dsc.scale = st.d_norm + norm_off[oi];
       dsc.shift = st.d_norm + norm_off[oi] + o.cout;
     }
-    if (o.kind == OP_LINEAR)
+    if ((o.kind == OP_LINEAR || o.kind == OP_CONV) && o.norm < 0 && o.tensor >= 0 &&
+        e->net.tensors[o.tensor].linear)  // bias (leading slice of the shared vector)
       dsc.shift = reinterpret_cast<const float*>(e->d_w + e->net.tensors[o.tensor].b_off);
     if (o.kind == OP_SE) dsc.aux = o.se_mid;
   }

@@ -30,6 +30,10 @@ enum OpKind : int {
   OP_GAP = 4,      // global average pool -> [N][C]
   OP_LINEAR = 5,   // classifier (fp32 logits)
   OP_SE = 6,       // squeeze-excite: x *= h_sigmoid(W2 relu(W1 gap(x) + b1) + b2)
+  OP_EMBED = 7,    // token + position + type embeddings -> LayerNorm
+  OP_ATTN = 8,     // softmax(Q K^T / sqrt(d)) V over the active heads
+  OP_LAYERNORM = 9,
+  OP_TOKEN0 = 10,  // gather position 0 of every sequence
 };
 
 // Logical buffer slots inside a block; mapped to arena buffers per graph.
@@ -42,9 +46,11 @@ enum Slot : int {
   S_T3 = 4,
   S_RAW = 5,     // input staging (raw host format)
   S_LOGITS = 6,  // fp32 logits
+  S_T4 = 7,
+  S_T5 = 8,
 };
 
-enum Act : int { ACT_NONE = 0, ACT_RELU = 1, ACT_HSWISH = 2 };
+enum Act : int { ACT_NONE = 0, ACT_RELU = 1, ACT_HSWISH = 2, ACT_GELU = 3, ACT_TANH = 4 };
 
 struct TensorSpec {
   int cout = 0, cin = 0, k = 1;  // max shape (depthwise: cin == 1)
@@ -69,7 +75,9 @@ struct OpSpec {
   int in = S_IN, out = S_OUT, res = S_NONE;
   bool res_post = false;  // residual added after the activation
   int tensor = -1, norm = -1;
-  int tensor2 = -1;            // OP_SE: expand tensor (tensor = reduce)
+  int tensor2 = -1;            // OP_SE: expand tensor (tensor = reduce); OP_EMBED: positions
+  int tensor3 = -1;            // OP_EMBED: token types
+  int in2 = S_NONE, in3 = S_NONE;  // OP_ATTN: K and V
   int se_mid = 0, se_mid_max = 0;
   int act = ACT_NONE;
   int stride = 1, k_max = 1, pool_k = 0;
@@ -213,11 +221,17 @@ inline void finalize_layout(Net& net) {
 }
 
 // Assign statistics slots to active norm layers in execution order.
+// SubnetNorm applies to BatchNorm-style norms only; LayerNorm (and the
+// embedding LN) normalise per token and keep no per-subnet statistics.
+inline bool has_subnet_norm(const OpSpec& o) {
+  return o.active && o.norm >= 0 && o.kind != OP_LAYERNORM && o.kind != OP_EMBED;
+}
+
 inline void assign_stats(Net& net) {
   uint64_t cursor = 0;
   int slot = 0;
   for (auto& o : net.ops) {
-    if (!o.active || o.norm < 0) continue;
+    if (!has_subnet_norm(o)) continue;
     o.stat_off = static_cast<int64_t>(cursor);
     o.norm_slot = slot++;
     cursor += static_cast<uint64_t>(o.cout);
@@ -806,11 +820,136 @@ inline Net build_ofa_mbv3(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
   return net;
 }
 
+// ---------------------------------------------------------------------------
+// Config 5 — width/depth-sliced BERT-base-like encoder (DESIGN.md §3.4,
+// [external] DynaBERT).  Post-LN layers: Q/K/V linears over the active heads,
+// softmax attention, output projection (+residual) -> LayerNorm, FFN with
+// GELU (+residual) -> LayerNorm; tanh pooler on token 0; classifier.
+//   D = 12 per-layer LayerSelect flags, E = [FFN width multiplier],
+//   W = [attention-head width multiplier] (heads_a = round(12 W), ffn_a =
+//   md(3072 E)).  desc.image_size = sequence length, num_classes = labels.
+// No BatchNorm: SubnetNorm statistics are empty for this family.
+
+inline Net build_bert(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
+  static const int HID = 768, HEADS = 12, HD = 64, FFN = 3072, LAYERS = 12, VOCAB = 30522;
+  SubnetCfg mx;
+  mx.depth.assign(LAYERS, 1);
+  mx.expand.assign(1, 1.0);
+  mx.width.assign(1, 1.0);
+  const SubnetCfg& s = cfg ? *cfg : mx;
+  if (s.depth.size() != LAYERS || s.expand.size() != 1 || s.width.size() != 1)
+    throw std::invalid_argument(
+        "bert subnet needs 12 depth flags, 1 FFN width (expand) ratio, 1 head width multiplier");
+  if (!(s.width[0] > 0.0) || s.width[0] > 1.0)
+    throw std::invalid_argument("width multiplier must be in (0,1]");
+  if (!(s.expand[0] > 0.0) || s.expand[0] > 1.0)
+    throw std::invalid_argument("FFN expand ratio must be in (0,1]");
+  if (d.dtype != SSN_DTYPE_BF16) throw std::invalid_argument("bert runs in bf16");
+  if (d.image_size != 128)  // attention kernel keeps one 128-token sequence per CTA
+    throw std::invalid_argument("bert sequence length (image_size) must be 128");
+  const int heads = std::max(1, rnd(HEADS * s.width[0]));
+  const int ffn = std::min(FFN, md8(FFN * s.expand[0]));
+  const int S = static_cast<int>(d.image_size);
+
+  Net net;
+  net.desc = d;
+  net.elem_bytes = 2;
+  Builder b(net);
+  // tensors (canonical ordinals): embeddings, then per layer q,k,v,o,f1,f2, pooler, classifier
+  const int t_tok = b.tensor(VOCAB, HID, 1, false, false);
+  const int t_pos = b.tensor(512, HID, 1, false, false);
+  const int t_typ = b.tensor(2, HID, 1, false, false);
+  const int n_emb = b.norm(HID);
+  auto lin = [&](int kind, int in, int out, int res, int t, int cin, int cin_max, int cout,
+                 int cout_max, int act) {
+    auto& o = b.op(kind);
+    o.in = in; o.out = out; o.res = res;
+    o.tensor = t; o.act = act;
+    o.hin = o.hout = S; o.win = o.wout = 1;
+    o.cin = cin; o.cin_max = cin_max; o.cout = cout; o.cout_max = cout_max;
+    return &o;
+  };
+  auto ln = [&](int in, int out, int nrm) {
+    auto& o = b.op(OP_LAYERNORM);
+    o.in = in; o.out = out; o.norm = nrm;
+    o.hin = o.hout = S; o.win = o.wout = 1;
+    o.cin = o.cin_max = o.cout = o.cout_max = HID;
+  };
+
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_EMBED);
+    o.in = S_RAW; o.out = S_OUT;
+    o.tensor = t_tok; o.tensor2 = t_pos; o.tensor3 = t_typ; o.norm = n_emb;
+    o.hin = o.hout = S; o.win = o.wout = 1;
+    o.cin = o.cin_max = 1;
+    o.cout = o.cout_max = HID;
+  }
+  b.end_block();
+  for (int l = 0; l < LAYERS; ++l) {
+    const int tq = b.tensor(HID, HID, 1, false, true);
+    const int tk = b.tensor(HID, HID, 1, false, true);
+    const int tv = b.tensor(HID, HID, 1, false, true);
+    const int to = b.tensor(HID, HID, 1, false, true);
+    const int n1 = b.norm(HID);
+    const int t1 = b.tensor(FFN, HID, 1, false, true);
+    const int t2 = b.tensor(HID, FFN, 1, false, true);
+    const int n2 = b.norm(HID);
+    b.begin_segment();
+    b.begin_block(l);
+    lin(OP_CONV, S_IN, S_T1, S_NONE, tq, HID, HID, heads * HD, HID, ACT_NONE);
+    lin(OP_CONV, S_IN, S_T2, S_NONE, tk, HID, HID, heads * HD, HID, ACT_NONE);
+    lin(OP_CONV, S_IN, S_T3, S_NONE, tv, HID, HID, heads * HD, HID, ACT_NONE);
+    {
+      auto& o = b.op(OP_ATTN);
+      o.in = S_T1; o.in2 = S_T2; o.in3 = S_T3; o.out = S_T4;
+      o.hin = o.hout = S; o.win = o.wout = 1;
+      o.cin = o.cout = heads * HD; o.cin_max = o.cout_max = HID;
+      o.k_max = o.k = HD;  // head dim
+    }
+    lin(OP_CONV, S_T4, S_T5, S_IN, to, heads * HD, HID, HID, HID, ACT_NONE);
+    ln(S_T5, S_T1, n1);
+    lin(OP_CONV, S_T1, S_T4, S_NONE, t1, HID, HID, ffn, FFN, ACT_GELU);
+    lin(OP_CONV, S_T4, S_T2, S_T1, t2, ffn, FFN, HID, HID, ACT_NONE);
+    ln(S_T2, S_OUT, n2);
+    b.end_block();
+  }
+  b.begin_segment();
+  b.begin_block(-1);
+  {
+    auto& o = b.op(OP_TOKEN0);  // [B][S][768] -> [B][768] (the [CLS] position)
+    o.hin = S; o.win = 1; o.hout = o.wout = 1;
+    o.cin = o.cin_max = o.cout = o.cout_max = HID;
+  }
+  b.end_block();
+  const int tp = b.tensor(HID, HID, 1, false, true);
+  b.begin_block(-1);
+  {
+    auto* o = lin(OP_CONV, S_IN, S_OUT, S_NONE, tp, HID, HID, HID, HID, ACT_TANH);
+    o->hin = o->hout = 1;
+  }
+  b.end_block();
+  const int tc = b.tensor(static_cast<int>(d.num_classes), HID, 1, false, true);
+  b.begin_block(-1);
+  {
+    auto* o = lin(OP_LINEAR, S_IN, S_LOGITS, S_NONE, tc, HID, HID, static_cast<int>(d.num_classes),
+                  static_cast<int>(d.num_classes), ACT_NONE);
+    o->hin = o->hout = 1;
+  }
+  b.end_block();
+  finalize_layout(net);
+  mark_blocks(net, s.depth);
+  assign_stats(net);
+  return net;
+}
+
 inline Net build_net(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
   switch (d.family) {
     case SSN_FAMILY_TINYCNN: return build_tinycnn(d, cfg);
     case SSN_FAMILY_OFA_RESNET50: return build_ofa_resnet50(d, cfg);
     case SSN_FAMILY_OFA_MBV3: return build_ofa_mbv3(d, cfg);
+    case SSN_FAMILY_BERT: return build_bert(d, cfg);
     default: throw std::invalid_argument("unsupported supernet family");
   }
 }

@@ -92,7 +92,8 @@ def ofa_resnet50_preset(name: str) -> SubnetConfig:
 # ---------------------------------------------------------------------------
 # plan accounting (algorithmic FLOPs / bytes per image)
 
-OP_KINDS = {0: "input", 1: "conv", 2: "maxpool", 3: "avgpool", 4: "gap", 5: "linear", 6: "se"}
+OP_KINDS = {0: "input", 1: "conv", 2: "maxpool", 3: "avgpool", 4: "gap", 5: "linear", 6: "se",
+            7: "embed", 8: "attn", 9: "layernorm", 10: "token0"}
 
 
 def plan_ops(desc, cfg: SubnetConfig):
@@ -146,6 +147,11 @@ def plan_cost(desc, cfg: SubnetConfig, elem_bytes: int = 2):
             b = hw_in * 3 * 4 + hw_out * r["cout"] * elem_bytes
         elif kind == "se":  # pool read + scale read/write of the activation
             b = 3 * hw_in * r["cin"] * elem_bytes
+        elif kind == "attn":  # QK^T and PV over the active heads, per sequence
+            f = 2 * 2 * hw_in * hw_in * r["cin"]
+            b = 4 * hw_in * r["cin"] * elem_bytes
+        elif kind == "embed":
+            b = hw_in * 4 + 2 * hw_out * r["cout"] * elem_bytes
         else:
             b = (hw_in * r["cin"] + hw_out * r["cout"]) * elem_bytes
         flops += f
@@ -175,4 +181,18 @@ def ofa_mbv3_preset(name: str) -> SubnetConfig:
 
 
 def preset(family: int, name: str) -> SubnetConfig:
+    if family == 4:
+        return {"min": bert_config(0.25, 0.5), "mid": bert_config(0.5, 0.75),
+                "max": bert_config(1.0, 1.0)}[name]
     return ofa_mbv3_preset(name) if family == 3 else ofa_resnet50_preset(name)
+
+
+BERT_DROP = {1.0: (), 0.75: (3, 7, 11), 0.5: (1, 3, 5, 7, 9, 11)}
+
+
+def bert_config(mw: float = 1.0, md: float = 1.0, ffn: float = None) -> SubnetConfig:
+    """DynaBERT-style (width mw, depth md) -> 12 layer flags, E = [FFN width],
+    W = [head width] (depth 0.75 drops layers 3/7/11, 0.5 the
+    odd layers)."""
+    drop = BERT_DROP[md]
+    return SubnetConfig([i not in drop for i in range(12)], [ffn if ffn else mw], [mw])

@@ -71,12 +71,14 @@ class Net:
     def __init__(self, seed, bf16):
         self.seed, self.bf16 = seed, bf16
         self.w, self.g, self.b, self.bias = [], [], [], []
+        self.bias_of = {}  # tensor ordinal -> bias
 
     def tensor(self, shape, linear=False):
         o = len(self.w)
         self.w.append(torch.from_numpy(weight(self.seed, o, shape, self.bf16)))
         if linear:
             self.bias.append(torch.from_numpy(0.1 * (2 * u01(self.seed, 4, o, np.arange(shape[0])) - 1)))
+            self.bias_of[o] = self.bias[-1]
         return o
 
     def norm(self, c, res=False):
@@ -273,6 +275,53 @@ def mbv3(seed):
     return forward, net
 
 
+def bert(seed, classes):
+    """Config 5: DynaBERT-style width/depth-sliced BERT-base."""
+    net = Net(seed, True)
+    t_tok, t_pos, t_typ = net.tensor((30522, 768)), net.tensor((512, 768)), net.tensor((2, 768))
+    n_emb = net.norm(768)
+    layers = []
+    for _ in range(12):
+        q, k, v, o = (net.tensor((768, 768), True) for _ in range(4))
+        n1 = net.norm(768)
+        f1, f2 = net.tensor((3072, 768), True), net.tensor((768, 3072), True)
+        layers.append((q, k, v, o, n1, f1, f2, net.norm(768)))
+    t_pool, t_cls = net.tensor((768, 768), True), net.tensor((classes, 768), True)
+
+    def lin(x, t, cout, cin=None):
+        w = net.w[t][:cout, :x.shape[-1] if cin is None else cin]
+        return F.linear(x, w, net.bias_of[t][:cout])
+
+    def ln(x, n):
+        return F.layer_norm(x, (768,), net.g[n], net.b[n], eps=1e-12)
+
+    def forward(cfg, ids):
+        flags, (fe,), (hw,) = cfg
+        heads = max(1, int(np.round(12 * hw)))
+        ffn = min(3072, md8(3072 * fe))
+        ca = heads * 64
+        ids = torch.from_numpy(ids.astype(np.int64))
+        nb, s = ids.shape
+        x = net.w[t_tok][ids] + net.w[t_pos][:s][None] + net.w[t_typ][0][None, None]
+        x = ln(x, n_emb)
+        for on, (q, k, v, o, n1, f1, f2, n2) in zip(flags, layers):
+            if not on:
+                continue
+            sp = lambda t: lin(x, t, ca).view(nb, s, heads, 64).transpose(1, 2)
+            att = torch.softmax(sp(q) @ sp(k).transpose(-1, -2) / 8.0, dim=-1) @ sp(v)
+            h = ln(lin(att.transpose(1, 2).reshape(nb, s, ca), o, 768) + x, n1)
+            x = ln(lin(F.gelu(lin(h, f1, ffn)), f2, 768) + h, n2)
+        pooled = torch.tanh(lin(x[:, 0], t_pool, 768))
+        return lin(pooled, t_cls, classes)
+
+    return forward
+
+
+def tokens(seed, ordinal, n, s):
+    return (u01(seed, 8, ordinal, np.arange(n * s)).astype(np.float64) * 30522).astype(
+        np.int32).reshape(n, s)
+
+
 def calibrate_and_forward(fwd, netobj, cfg, cal_x, x):
     r = Run(netobj, True)
     fwd(r, cfg, torch.from_numpy(cal_x))
@@ -321,6 +370,19 @@ def main():
         m, v, lg = calibrate_and_forward(fwd, netobj, cfg, cal_x, x)
         out[f"mb_{name}_mean"], out[f"mb_{name}_var"], out[f"mb_{name}_logits"] = m, v, lg
     out["mb_cfgs"] = np.array(repr(mb_cfgs))
+    # ---- width/depth-sliced BERT (config 5), seq 32, 4 classes, bf16-valued weights
+    bert_cfgs = {
+        "min": ([i not in (1, 3, 5, 7, 9, 11) for i in range(12)], [0.25], [0.25]),
+        "mid": ([i not in (3, 7, 11) for i in range(12)], [0.5], [0.5]),
+        "max": ([True] * 12, [1.0], [1.0]),
+    }
+    fwd = bert(seed, 4)
+    ids = tokens(seed, 1, 2, 32)
+    out["bert_ids"] = ids
+    with torch.no_grad():
+        for name, cfg in bert_cfgs.items():
+            out[f"bert_{name}_logits"] = fwd(cfg, ids).numpy()
+    out["bert_cfgs"] = np.array(repr(bert_cfgs))
     # ---- operator fixtures: WeightSlice conv with slices, crop, depthwise
     rng = np.random.default_rng(0)
     ops = []

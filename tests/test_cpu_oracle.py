@@ -188,3 +188,45 @@ def test_mbv3_survey_numbers(mb_oracle):
         ssn.plan_stat_count(d, ssn.SubnetConfig([True] * 10, [3.0] * 20, [1.0], [4] * 20))
     with pytest.raises(ValueError, match="fixed width"):
         ssn.plan_stat_count(d, ssn.SubnetConfig([True] * 10, [3.0] * 20, [0.5], [3] * 20))
+
+
+# ---------------------------------------------------------------- config 5: BERT
+BERT = {k: ssn.SubnetConfig(*map(list, v))
+        for k, v in ast.literal_eval(str(GOLD["bert_cfgs"])).items()}
+
+
+@pytest.fixture(scope="module")
+def bert_oracle():
+    return O.OracleNet(ssn.FAMILY_BERT, seed=0, classes=4, bf16_weights=True)
+
+
+def test_bert_tokens_match_rng_spec():
+    np.testing.assert_array_equal(O.tokens(0, 1, 2, 32), GOLD["bert_ids"])
+
+
+@pytest.mark.parametrize("name", list(BERT))
+def test_oracle_bert_matches_torch(bert_oracle, name):
+    """Head/FFN WeightSlice + LayerSelect over layers vs torch F.linear /
+    layer_norm / softmax attention (make_golden.py bert())."""
+    lg = bert_oracle.forward_tokens(BERT[name], GOLD["bert_ids"])
+    ref = GOLD[f"bert_{name}_logits"]
+    assert rel(lg, ref) < 1e-4, rel(lg, ref)
+
+
+def test_bert_plan_and_validation(bert_oracle):
+    d = ssn.make_desc(ssn.FAMILY_BERT, image_size=128, num_classes=2)
+    for cfg in BERT.values():
+        assert ssn.plan_stat_count(d, cfg) == 0 == bert_oracle.stat_count(cfg)  # LayerNorm only
+    # BERT-base at seq 128: ~22.3 GFLOP per sequence for the full encoder
+    full = ssn.plan_cost(d, ssn.bert_config(1.0, 1.0))["flops"] / 1e9
+    assert 21.5 < full < 23.0, full
+    half = ssn.plan_cost(d, ssn.bert_config(0.5, 0.5))["flops"] / 1e9
+    assert half < full / 3
+    with pytest.raises(ValueError, match="12 depth flags"):
+        ssn.plan_stat_count(d, ssn.SubnetConfig([True] * 11, [1.0], [1.0]))
+    with pytest.raises(ValueError, match="width multiplier"):
+        ssn.plan_stat_count(d, ssn.SubnetConfig([True] * 12, [1.0], [1.5]))
+    with pytest.raises(ValueError, match="must be 128"):
+        ssn.plan_stat_count(ssn.make_desc(ssn.FAMILY_BERT, image_size=64), BERT["max"])
+    with pytest.raises(ValueError, match="12 depth flags"):
+        bert_oracle.forward_tokens(ssn.SubnetConfig([True] * 3, [1.0], [1.0]), GOLD["bert_ids"])

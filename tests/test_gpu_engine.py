@@ -227,3 +227,43 @@ def test_ofa_mbv3_bf16_parity(mbv3, name):
     assert e_emu <= 2e-2
     assert e_ref <= 2e-2
     argmax_agree(got, ref, tol=4 * e_ref * np.abs(ref).max())
+
+
+# ---------------------------------------------------------------- config 5: BERT
+BERT_CASES = {
+    "min": ssn.bert_config(0.25, 0.5),
+    "mid": ssn.bert_config(0.5, 0.75),
+    "max": ssn.bert_config(1.0, 1.0),
+    "mixed": ssn.SubnetConfig([True, False, True, True, False, False, True, True, False, True,
+                               False, True], [0.4], [0.75]),
+}
+
+
+@pytest.fixture(scope="module")
+def bert(gpu):
+    desc = ssn.make_desc(ssn.FAMILY_BERT, ssn.DTYPE_BF16, image_size=128, num_classes=8,
+                         max_batch=8, seed=SEED)
+    eng = ssn.Engine(desc)
+    on = O.OracleNet(ssn.FAMILY_BERT, seed=SEED, classes=8, bf16_weights=True)
+    for sid, cfg in enumerate(BERT_CASES.values()):
+        eng.register_subnet(sid, cfg)
+    eng.prepare([4, 8])
+    yield eng, on
+    eng.close()
+
+
+@pytest.mark.parametrize("name", list(BERT_CASES))
+def test_bert_bf16_parity(bert, name):
+    """Config 5: head/FFN WeightSlice, per-layer LayerSelect, seq 128."""
+    eng, on = bert
+    cfg = BERT_CASES[name]
+    ids = O.tokens(SEED, 3, 6, 128)
+    eng.actuate(list(BERT_CASES).index(name))
+    got = eng.infer(ids, 6, 8)  # 6 live sequences padded to the bs-8 graph
+    emu = on.forward_tokens(cfg, ids, bf16_storage=True)
+    ref = on.forward_tokens(cfg, ids)
+    e_emu, e_ref = rel(got, emu), rel(got, ref)
+    print(f"bert {name}: rel vs bf16-storage oracle {e_emu:.2e}, vs fp32 oracle {e_ref:.2e}")
+    assert e_emu <= 2e-2
+    assert e_ref <= 4e-2
+    argmax_agree(got, emu, tol=4 * e_emu * np.abs(emu).max())
