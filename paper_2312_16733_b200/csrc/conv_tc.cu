@@ -167,21 +167,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // everything that does not depend on the accumulator is issued first
         const int col = n0 + cc + seg * 8;
         const bool colok = col < d.cout && cc + seg * 8 < bn;
+        // 8-wide vector path unless this is the ragged tail of a cout % 8 != 0
+        // slice (e.g. a 2-label classifier): then scalar loads and stores.
+        const int nv = colok ? min(8, d.cout - col) : 0;
+        const bool vec = nv == 8 && (d.cout & 7) == 0;
         float sc[8], sh[8];
         uint4 rv[4];
         if (colok) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            sc[q] = scale ? __ldg(scale + col + q) : 1.f;
-            sh[q] = shift ? __ldg(shift + col + q) : 0.f;
+            sc[q] = scale && q < nv ? __ldg(scale + col + q) : 1.f;
+            sh[q] = shift && q < nv ? __ldg(shift + col + q) : 0.f;
           }
           if (p.res) {
 #pragma unroll
             for (int r4 = 0; r4 < 4; ++r4) {
               const int m = m0 + rsub + 8 * r4;
-              if (m < p.M)
-                rv[r4] = __ldg(reinterpret_cast<const uint4*>(
-                    static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col));
+              if (m >= p.M) continue;
+              const __nv_bfloat16* rp =
+                  static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col;
+              if (vec) {
+                rv[r4] = __ldg(reinterpret_cast<const uint4*>(rp));
+              } else {
+                __nv_bfloat16* rs = reinterpret_cast<__nv_bfloat16*>(&rv[r4]);
+                for (int q = 0; q < 8; ++q) rs[q] = q < nv ? rp[q] : __float2bfloat16(0.f);
+              }
             }
           }
         }
@@ -230,7 +240,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               for (int q = 0; q < 8; ++q) o[q] += r8[q];
             }
             const size_t off = static_cast<size_t>(m) * d.cout + col;
-            if (p.out_f32) {
+            if (!vec) {
+              for (int q = 0; q < nv; ++q) {
+                if (p.out_f32)
+                  static_cast<float*>(p.y)[off + q] = o[q];
+                else
+                  static_cast<__nv_bfloat16*>(p.y)[off + q] = __float2bfloat16_rn(o[q]);
+              }
+            } else if (p.out_f32) {
               float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + off);
               yp[0] = make_float4(o[0], o[1], o[2], o[3]);
               yp[1] = make_float4(o[4], o[5], o[6], o[7]);

@@ -105,7 +105,16 @@ struct SubnetState {
   uint64_t norm_bytes = 0;
   uint64_t stat_bytes = 0;
   std::vector<uint32_t> seg_mask;
+  // Per segment: graph variant (LayerSelect mask | SEG_FLIP when the input sits
+  // in the other boundary buffer because an earlier segment ran no block) and
+  // whether any block of the segment runs at all.
+  std::vector<uint32_t> seg_var;
+  std::vector<uint8_t> seg_run;
 };
+
+// Variant bit: the segment's input is in the boundary buffer of the opposite
+// parity (an earlier segment was skipped entirely and passed its input on).
+constexpr uint32_t SEG_FLIP = 1u << 15;
 
 struct ssn_engine {
   int device = 0;
@@ -378,8 +387,10 @@ struct SlotMap {
 // The ops one LayerSelect variant of a segment runs, each with its slot ->
 // arena-buffer mapping (used by graph capture AND by ssn_register_subnet to
 // encode each op's activation TMA map over the buffer it will really read).
-static std::vector<SlotMap> segment_plan(const ssn_engine* e, int seg, uint32_t mask) {
+static std::vector<SlotMap> segment_plan(const ssn_engine* e, int seg, uint32_t variant) {
   const SegmentSpec& S = e->net.segments[seg];
+  const bool flip = (variant & SEG_FLIP) != 0;
+  const uint32_t mask = variant & ~SEG_FLIP;
   std::vector<int> act;
   for (int bi : S.blocks) {
     const BlockSpec& b = e->net.blocks[bi];
@@ -390,8 +401,9 @@ static std::vector<SlotMap> segment_plan(const ssn_engine* e, int seg, uint32_t 
     }
     if (on) act.push_back(bi);
   }
-  const int in_bnd = seg % 2 == 0 ? B_BND0 : B_BND1;
-  const int out_bnd = seg % 2 == 0 ? B_BND1 : B_BND0;
+  const bool even = (seg % 2 == 0) != flip;
+  const int in_bnd = even ? B_BND0 : B_BND1;
+  const int out_bnd = even ? B_BND1 : B_BND0;
   const int k = static_cast<int>(act.size());
   int cur_in = in_bnd;
   std::vector<SlotMap> out;
@@ -486,15 +498,24 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     CUDA_TRY(cudaMalloc(&st.d_norm, st.norm_bytes));
     CUDA_TRY(cudaMemcpy(st.d_norm, norm.data(), st.norm_bytes, cudaMemcpyHostToDevice));
   }
-  st.seg_mask.assign(e->net.segments.size(), 0);
-  for (size_t si = 0; si < e->net.segments.size(); ++si)
+  const size_t nseg = e->net.segments.size();
+  st.seg_mask.assign(nseg, 0);
+  st.seg_var.assign(nseg, 0);
+  st.seg_run.assign(nseg, 0);
+  for (size_t si = 0; si < nseg; ++si)
     for (size_t f = 0; f < e->net.segments[si].flags.size(); ++f)
       if (cfg.depth[e->net.segments[si].flags[f]]) st.seg_mask[si] |= 1u << f;
-  // physical input buffer of every op this subnet runs
+  // physical input buffer of every op this subnet runs; a segment whose
+  // blocks are all skipped (LayerSelect) leaves its input where it is.
   std::vector<const void*> in_ptr(st.plan.ops.size(), nullptr);
-  for (size_t si = 0; si < e->net.segments.size(); ++si)
-    for (const SlotMap& sm : segment_plan(e, static_cast<int>(si), st.seg_mask[si]))
-      in_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in, sm.map);
+  bool flip = false;
+  for (size_t si = 0; si < nseg; ++si) {
+    st.seg_var[si] = st.seg_mask[si] | (flip ? SEG_FLIP : 0u);
+    const auto sp = segment_plan(e, static_cast<int>(si), st.seg_var[si]);
+    st.seg_run[si] = !sp.empty();
+    if (sp.empty()) flip = !flip;
+    for (const SlotMap& sm : sp) in_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in, sm.map);
+  }
   std::vector<OpDesc> row(st.plan.ops.size());
   for (size_t oi = 0; oi < st.plan.ops.size(); ++oi) {
     const OpSpec& o = st.plan.ops[oi];
@@ -616,6 +637,8 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     e->desc = *desc;
     e->bf16 = desc->dtype == SSN_DTYPE_BF16;
     e->net = build_net(*desc, nullptr);
+    for (const SegmentSpec& sg : e->net.segments)
+      if (sg.flags.size() >= 15) SSN_THROW(SSN_E_INVALID, "too many LayerSelect flags in a segment");
     CUDA_TRY(cudaSetDevice(device));
     int major = 0, minor = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
@@ -721,9 +744,15 @@ int ssn_prepare(ssn_engine* e, const uint32_t* batch_grid, uint32_t n) {
     for (uint32_t i = 0; i < n; ++i) {
       const uint32_t b = batch_grid[i];
       if (std::find(e->grid.begin(), e->grid.end(), b) != e->grid.end()) continue;
+      bool can_flip = false;  // some earlier segment may run no block at all
       for (size_t si = 0; si < e->net.segments.size(); ++si) {
         const uint32_t variants = 1u << e->net.segments[si].flags.size();
-        for (uint32_t m = 0; m < variants; ++m) build_graph(e, static_cast<int>(si), m, b);
+        for (uint32_t f = 0; f <= (can_flip ? 1u : 0u); ++f)
+          for (uint32_t m = 0; m < variants; ++m)
+            build_graph(e, static_cast<int>(si), m | (f ? SEG_FLIP : 0u), b);
+        bool all_optional = true;
+        for (int bi : e->net.segments[si].blocks) all_optional &= e->net.blocks[bi].flag >= 0;
+        can_flip |= all_optional;
       }
       e->grid.push_back(b);
     }
@@ -770,7 +799,8 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
     }
     if (x) CUDA_TRY(cudaMemcpyAsync(e->d_raw, x, e->raw_img_bytes * count, cudaMemcpyDefault, s));
     for (size_t si = 0; si < e->net.segments.size(); ++si) {
-      auto it = e->graphs.find(graph_key(static_cast<int>(si), sub.seg_mask[si], profiled_batch));
+      if (!sub.seg_run[si]) continue;  // every block skipped: input passes through
+      auto it = e->graphs.find(graph_key(static_cast<int>(si), sub.seg_var[si], profiled_batch));
       if (it == e->graphs.end()) SSN_THROW(SSN_E_STATE, "missing graph segment");
       CUDA_TRY(cudaGraphLaunch(it->second.first, s));
       kernels += static_cast<uint32_t>(it->second.second);
@@ -843,7 +873,7 @@ int ssn_profile_ops(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t iters, 
     for (uint32_t it = 0; it < iters + 1; ++it) {  // first pass = warm-up
       std::vector<bool> ran(nop, false);
       for (size_t si = 0; si < e->net.segments.size(); ++si)
-        enqueue_segment(e, static_cast<int>(si), sub.seg_mask[si], batch, s, [&](int op, bool before) {
+        enqueue_segment(e, static_cast<int>(si), sub.seg_var[si], batch, s, [&](int op, bool before) {
           CUDA_TRY(cudaEventRecord(ev[2 * op + (before ? 0 : 1)], s));
           ran[op] = true;
         });

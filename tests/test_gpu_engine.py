@@ -236,6 +236,7 @@ BERT_CASES = {
     "max": ssn.bert_config(1.0, 1.0),
     "mixed": ssn.SubnetConfig([True, False, True, True, False, False, True, True, False, True,
                                False, True], [0.4], [0.75]),
+    "no_layers": ssn.SubnetConfig([False] * 12, [1.0], [1.0]),  # every segment passes through
 }
 
 

@@ -92,6 +92,15 @@ def test_conv_bf16_residual_and_f32_out(gpu):
     assert np.abs(got - ref).max() / np.abs(ref).max() < 5e-3
 
 
+@pytest.mark.parametrize("cout", [2, 10, 13])
+def test_conv_bf16_ragged_cout(gpu, cout):
+    """cout % 8 != 0 (e.g. a 2-label classifier) takes the scalar epilogue tail."""
+    got, ref = _run_bf16(gpu, 16, 1, 1, 768, 768, cout, 16, 1, 1, act=0, out_f32=True)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 5e-3
+    got, ref = _run_bf16(gpu, 2, 6, 6, 64, 64, cout, 16, 3, 1, res=True, act=1)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-2
+
+
 def test_conv_bf16_rejects_bad_slices(gpu):
     import torch
     x = torch.zeros(64, device=gpu, dtype=torch.bfloat16)
