@@ -55,7 +55,32 @@ struct TcCfg {
       1024 + STAGES * (A_BYTES + B_BYTES) + TC_STG_BYTES + (2 * STAGES + 2 * NACC) * 8 + 16;
 };
 
-template <int BN_MAX, int STAGES>
+// Ragged tail of a cout % 8 != 0 slice (e.g. a 2-label classifier): scalar
+// accesses, kept out of line so the 8-wide vector epilogue stays compact.
+static __device__ __noinline__ uint4 load_ragged_bf16x8(const __nv_bfloat16* rp, int nv) {
+  uint4 r = make_uint4(0, 0, 0, 0);
+  __nv_bfloat16* rs = reinterpret_cast<__nv_bfloat16*>(&r);
+  for (int q = 0; q < nv; ++q) rs[q] = rp[q];
+  return r;
+}
+
+static __device__ __noinline__ void store_ragged8(void* y, size_t off, int nv, int out_f32, float o0,
+                                                  float o1, float o2, float o3, float o4, float o5,
+                                                  float o6, float o7) {
+  const float o[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
+  for (int q = 0; q < nv; ++q) {
+    if (out_f32)
+      static_cast<float*>(y)[off + q] = o[q];
+    else
+      static_cast<__nv_bfloat16*>(y)[off + q] = __float2bfloat16_rn(o[q]);
+  }
+}
+
+// EPI: 0 = identity/ReLU (the CNNs), 1 = h_swish (MBv3), 2 = GELU / tanh or a
+// ragged output slice (cout % 8 != 0; BERT head).  One instance per epilogue
+// keeps each compact: an inlined erff/tanhf + scalar tail tripled the SASS of
+// the ReLU kernel and halved its throughput through I-cache misses.
+template <int BN_MAX, int STAGES, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
   using C = TcCfg<BN_MAX, STAGES>;
@@ -170,14 +195,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // 8-wide vector path unless this is the ragged tail of a cout % 8 != 0
         // slice (e.g. a 2-label classifier): then scalar loads and stores.
         const int nv = colok ? min(8, d.cout - col) : 0;
-        const bool vec = nv == 8 && (d.cout & 7) == 0;
+        const bool vec = EPI != 2 || (nv == 8 && (d.cout & 7) == 0);
         float sc[8], sh[8];
         uint4 rv[4];
         if (colok) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            sc[q] = scale && q < nv ? __ldg(scale + col + q) : 1.f;
-            sh[q] = shift && q < nv ? __ldg(shift + col + q) : 0.f;
+            const int cq = EPI == 2 ? min(col + q, d.cout - 1) : col + q;  // ragged: clamp
+            sc[q] = scale ? __ldg(scale + cq) : 1.f;
+            sh[q] = shift ? __ldg(shift + cq) : 0.f;
           }
           if (p.res) {
 #pragma unroll
@@ -186,12 +212,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (m >= p.M) continue;
               const __nv_bfloat16* rp =
                   static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col;
-              if (vec) {
-                rv[r4] = __ldg(reinterpret_cast<const uint4*>(rp));
-              } else {
-                __nv_bfloat16* rs = reinterpret_cast<__nv_bfloat16*>(&rv[r4]);
-                for (int q = 0; q < 8; ++q) rs[q] = q < nv ? rp[q] : __float2bfloat16(0.f);
-              }
+              rv[r4] = vec ? __ldg(reinterpret_cast<const uint4*>(rp)) : load_ragged_bf16x8(rp, nv);
             }
           }
         }
@@ -231,7 +252,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int q = 0; q < 8; ++q) o[q] += r8[q];
               }
             }
-            if (p.act) {
+            if (p.act == 1) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
+            } else if (EPI == 1 && p.act == 2) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] *= fminf(fmaxf(o[q] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+            } else if (EPI == 2 && p.act) {
 #pragma unroll
               for (int q = 0; q < 8; ++q) o[q] = act_apply(o[q], p.act);
             }
@@ -241,12 +268,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             const size_t off = static_cast<size_t>(m) * d.cout + col;
             if (!vec) {
-              for (int q = 0; q < nv; ++q) {
-                if (p.out_f32)
-                  static_cast<float*>(p.y)[off + q] = o[q];
-                else
-                  static_cast<__nv_bfloat16*>(p.y)[off + q] = __float2bfloat16_rn(o[q]);
-              }
+              store_ragged8(p.y, off, nv, p.out_f32, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
             } else if (p.out_f32) {
               float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + off);
               yp[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -403,12 +425,16 @@ int choose_bn(int cout_max, long M) {
 #define SSN_TC_INSTANCES(X) X(64, 7) X(128, 5) X(256, 3)
 
 cudaError_t init_conv_tc() {
-#define SSN_TC_ATTR(BN, ST)                                                           \
-  {                                                                                   \
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN, ST>,                      \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         TcCfg<BN, ST>::SMEM);                        \
-    if (e != cudaSuccess) return e;                                                   \
+#define SSN_TC_ATTR(BN, ST)                                                             \
+  {                                                                                     \
+    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, 0>,               \
+                                               conv_tc_kernel<BN, ST, 1>,               \
+                                               conv_tc_kernel<BN, ST, 2>};              \
+    for (auto fn : fns) {                                                               \
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           TcCfg<BN, ST>::SMEM);                        \
+      if (e != cudaSuccess) return e;                                                   \
+    }                                                                                   \
   }
   SSN_TC_INSTANCES(SSN_TC_ATTR)
 #undef SSN_TC_ATTR
@@ -420,7 +446,12 @@ static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cud
   using C = TcCfg<BN_MAX, STAGES>;
   const long tiles = static_cast<long>((p.M + TC_BM - 1) / TC_BM) * ((p.cout_max + p.bn - 1) / p.bn);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  conv_tc_kernel<BN_MAX, STAGES><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+  if (p.act > 2 || (p.cout_max & 7) != 0 || p.ragged)
+    conv_tc_kernel<BN_MAX, STAGES, 2><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+  else if (p.act == 2)
+    conv_tc_kernel<BN_MAX, STAGES, 1><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+  else
+    conv_tc_kernel<BN_MAX, STAGES, 0><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   return cudaGetLastError();
 }
 

@@ -27,13 +27,20 @@ struct alignas(64) OpDesc {
   int aux;             // OP_SE: active squeeze width
 };
 
+// GELU / tanh are out of line: inlined into the unrolled GEMM epilogues their
+// erff/tanhf bodies tripled the conv kernel's SASS and thrashed the I-cache.
+static __device__ __noinline__ float act_apply_cold(float v, int act) {
+  if (act == 3) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));  // GELU (erf)
+  if (act == 4) return tanhf(v);
+  return v;
+}
+
 // h_swish(x) = x * relu6(x + 3) / 6 ; h_sigmoid(x) = relu6(x + 3) / 6
 __device__ __forceinline__ float act_apply(float v, int act) {
   if (act == 1) return fmaxf(v, 0.f);
   if (act == 2) return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
-  if (act == 3) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));  // GELU (erf)
-  if (act == 4) return tanhf(v);
-  return v;
+  if (act == 0) return v;
+  return act_apply_cold(v, act);
 }
 
 // Transformer ops (config 5): token embedding + LayerNorm, attention, LayerNorm
@@ -102,6 +109,7 @@ struct ConvParams {
   int k_max, cin_max, cout_max;
   int act, res_post, out_f32, depthwise;
   int bn;             // N tile (tcgen05 path)
+  int ragged;         // some active cout may be % 8 != 0 (scalar epilogue tail)
 };
 
 

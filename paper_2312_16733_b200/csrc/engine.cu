@@ -960,9 +960,10 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
                      void* stream) {
   return guarded([&] {
     if (!x || !wgt || !y) SSN_THROW(SSN_E_INVALID, "null tensor");
-    if (cin % 8 || cin_max % 8 || cout % 8 || cin > cin_max || cout > cout_max || cin <= 0 ||
-        cout <= 0)
-      SSN_THROW(SSN_E_INVALID, "channel counts must be positive multiples of 8 within max shape");
+    // input channels feed 16-byte TMA strides; the output slice may be ragged
+    // (the epilogue's scalar tail handles cout % 8 != 0, e.g. a 2-label head)
+    if (cin % 8 || cin_max % 8 || cin > cin_max || cout > cout_max || cin <= 0 || cout <= 0)
+      SSN_THROW(SSN_E_INVALID, "input channels must be positive multiples of 8 within max shape");
     if (k < 1 || stride < 1 || pad < 0) SSN_THROW(SSN_E_INVALID, "bad geometry");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(init_conv_tc());
@@ -990,6 +991,7 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.res_post = 0;
     p.out_f32 = out_f32;
     p.bn = choose_bn(cout_max, p.M);
+    p.ragged = (cout & 7) != 0;
     CUtensorMap wmap{};
     if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
