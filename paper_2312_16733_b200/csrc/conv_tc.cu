@@ -6,7 +6,7 @@
 //   PAPER.md:472-481 SubnetNorm folded into the epilogue).
 //
 // Design:
-//  * Both operands move by TMA, issued by ONE producer thread per CTA:
+//  * Both operands move by TMA:
 //      A (activations): TMA im2col mode — one cp.async.bulk.tensor.4d.im2col
 //        per K block loads 128 consecutive output pixels x 64 channels of one
 //        filter tap; padding, channel tails (> cin_a) and the batch tail are
@@ -18,13 +18,19 @@
 //        its LEADING slice — no copy of any slice ever exists.
 //    Both land 128B-swizzled (SW128 K-major), the layout tcgen05.mma reads.
 //  * Persistent and warp-specialised: one CTA per SM walks a static tile
-//    schedule; warp 0 produces, warp 9 issues tcgen05.mma (one thread), warps
-//    1-8 drain.  Accumulators live in a TMEM ring (NACC buffers of BN_MAX fp32
-//    columns), so several tiles are in flight between MMA and epilogue.
+//    schedule; warp 0 produces, warp 9 issues tcgen05.mma, warps 1-8 drain.
+//    Producer and MMA loops run warp-wide and elect one lane to issue, so the
+//    descriptors stay warp-uniform (a lane-0-only loop wrapped every
+//    UTCHMMA/UTMALDG in a divergent R2UR waterfall: 500 vs 360 cycles per
+//    K block measured, tools/ubench/tc_loop.cu).
+//  * A ring stage holds KPS K blocks (the per-stage mbarrier wait + commit
+//    costs ~150-250 cycles, as much as four N=96 MMAs).
+//  * Accumulators live in a TMEM ring (NACC buffers of BN_MAX fp32 columns),
+//    so several tiles are in flight between MMA and epilogue.
 //  * Epilogue: two groups of 4 warps take alternate tiles; each warp
 //    tcgen05.ld's 32 TMEM lanes x 32 columns, transposes through padded smem,
-//    then applies SubnetNorm scale/shift, residual and ReLU on coalesced
-//    64-byte row segments and stores bf16 (or fp32 logits).
+//    then applies SubnetNorm scale/shift, residual and the activation on
+//    coalesced 64-byte row segments and stores bf16 (or fp32 logits).
 //  * Subnet extents (cin_a, cout_a, k_a, SubnetNorm row, activation map) come
 //    from the actuated subnet's descriptor, so one graph-captured launch
 //    serves every subnet; the tile count follows cout_a on the device.
@@ -39,21 +45,31 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_PROD_WARP = 0;
-constexpr int TC_MMA_WARP = 1 + TC_EPI_WARPS;   // 9
+constexpr int TC_MMA_WARP = 1 + TC_EPI_WARPS;       // 9
 constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 320
 constexpr int TC_STG_LD = 36;  // padded fp32 row of the 32x32 epilogue transpose tile
 constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
 
-template <int BN_MAX, int STAGES>
+template <int BN_MAX, int STAGES, int KPS>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN_MAX * TC_BK * 2;
+  static constexpr int STAGE_BYTES = KPS * (A_BYTES + B_BYTES);
   // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
   // (max 4), so the MMA can run several tiles ahead of the epilogue.
   static constexpr int NACC = 512 / BN_MAX > 4 ? 4 : 512 / BN_MAX;
   static constexpr int SMEM =
-      1024 + STAGES * (A_BYTES + B_BYTES) + TC_STG_BYTES + (2 * STAGES + 2 * NACC) * 8 + 16;
+      1024 + STAGES * STAGE_BYTES + TC_STG_BYTES + (2 * STAGES + 2 * NACC) * 8 + 16;
+  static_assert(SMEM <= 232448, "operand ring exceeds 227 KB of shared memory");
 };
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 
 // Ragged tail of a cout % 8 != 0 slice (e.g. a 2-label classifier): scalar
 // accesses, kept out of line so the 8-wide vector epilogue stays compact.
@@ -76,22 +92,31 @@ static __device__ __noinline__ void store_ragged8(void* y, size_t off, int nv, i
   }
 }
 
+// Per-chunk epilogue operands (SubnetNorm scale/shift of 8 columns, residual
+// of 4 rows x 8 columns), fetched one chunk ahead.
+struct EpiIn {
+  float sc[8];
+  float sh[8];
+  uint4 rv[4];
+};
+
 // EPI: 0 = identity/ReLU (the CNNs), 1 = h_swish (MBv3), 2 = GELU / tanh or a
 // ragged output slice (cout % 8 != 0; BERT head).  One instance per epilogue
 // keeps each compact: an inlined erff/tanhf + scalar tail tripled the SASS of
 // the ReLU kernel and halved its throughput through I-cache misses.
-template <int BN_MAX, int STAGES, int EPI>
+template <int BN_MAX, int STAGES, int KPS, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
-  using C = TcCfg<BN_MAX, STAGES>;
+  using C = TcCfg<BN_MAX, STAGES, KPS>;
   constexpr int NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * C::A_BYTES;
-  float* epi_stage = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES + TC_STG_BYTES);
+  // 1024-B aligned for SW128; offset arithmetic on smem_raw keeps the shared
+  // address space visible to the compiler
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;                                 // [STAGES][KPS] A boxes
+  uint8_t* sB = smem + STAGES * KPS * C::A_BYTES;     // [STAGES][KPS] B boxes
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES + TC_STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [NACC]
   uint64_t* tempty = tfull + NACC;   // [NACC]
@@ -128,197 +153,292 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
+  const bool prof = (p.dbg & 32) && blockIdx.x == 0;
+  long long w_wait = 0, w_wait2 = 0;
+  const long long t_begin = prof ? clock64() : 0;
 
   if (warp == TC_PROD_WARP) {
     // ============================================================ producer
-    if (lane == 0) {
-      const CUtensorMap* amap = &dp->amap;
-      const int hwo = p.ho * p.wo;
-      const uint32_t tx = static_cast<uint32_t>(C::A_BYTES + bn * TC_BK * 2);
-      int g = 0;  // global K-block counter (ring position)
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t / nt) * TC_BM;
-        const int n0 = (t % nt) * bn;
-        const int img = m0 / hwo;
-        const int rem = m0 - img * hwo;
-        const int oh = rem / p.wo;
-        const int ow = rem - oh * p.wo;
-        const int w0 = ow * p.stride - pad, h0 = oh * p.stride - pad;
-        int tr = 0, ts = 0, cb = 0;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % STAGES;
-          const uint32_t ph = (g / STAGES) & 1;
+    const bool leader = elect_one();
+    const CUtensorMap* amap = &dp->amap;
+    const int hwo = p.ho * p.wo;
+    const uint32_t kb_bytes = static_cast<uint32_t>(C::A_BYTES + bn * TC_BK * 2);
+    int g = 0;  // stage counter (ring position)
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t / nt) * TC_BM;
+      const int n0 = (t % nt) * bn;
+      const int img = m0 / hwo;
+      const int rem = m0 - img * hwo;
+      const int oh = rem / p.wo;
+      const int ow = rem - oh * p.wo;
+      const int w0 = ow * p.stride - pad, h0 = oh * p.stride - pad;
+      int tr = 0, ts = 0, cb = 0;
+      for (int kb = 0; kb < nk; kb += KPS, ++g) {
+        const int s = g % STAGES;
+        const uint32_t ph = (g / STAGES) & 1;
+        if (prof) {
+          const long long t0 = clock64();
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], tx);
-          tma_im2col_4d(sA + s * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0, img,
-                        static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
-          tma_load_3d(sB + s * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
-                      (tr + koff) * p.k_max + (ts + koff), n0);
-          if (++cb == cblocks) {
-            cb = 0;
-            if (++ts == ka) {
-              ts = 0;
-              ++tr;
+          w_wait += clock64() - t0;
+        } else {
+          mbar_wait(&empty[s], ph ^ 1);
+        }
+        const int nsub = min(KPS, nk - kb);
+        if (leader) {
+          const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES);
+          const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
+          const uint32_t tx = (p.dbg & 12) ? nsub * (a_tx + b_tx) : nsub * kb_bytes;
+          if (tx) mbar_arrive_expect_tx(&full[s], tx);
+          else mbar_arrive(&full[s]);
+        }
+#pragma unroll
+        for (int j = 0; j < KPS; ++j) {
+          if (j < nsub) {
+            if (leader) {
+              if (!(p.dbg & 4))
+                tma_im2col_4d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0,
+                              img, static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
+              if (!(p.dbg & 8))
+                tma_load_3d(sB + (s * KPS + j) * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
+                            (tr + koff) * p.k_max + (ts + koff), n0);
+            }
+            if (++cb == cblocks) {
+              cb = 0;
+              if (++ts == ka) {
+                ts = 0;
+                ++tr;
+              }
             }
           }
         }
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else if (warp < TC_MMA_WARP) {
     // ============================================================ epilogue
     // TMEM gives each thread one ROW; global memory wants each warp to touch
     // whole row segments.  Each 32x32 fp32 chunk is transposed through a
     // per-warp padded smem tile: afterwards lane (rsub = lane/4, seg = lane%4)
     // owns 8 consecutive columns of rows rsub, rsub+8, ... so residual loads
-    // and output stores are 64-byte row-contiguous and coalesced.  Two groups
-    // (4 warps each, one per TMEM lane quarter) take alternate tiles.
+    // and output stores are 64-byte row-contiguous and coalesced (a
+    // row-per-lane epilogue without the transpose measured 1.6x slower on the
+    // HBM-bound 1x1 convs).  Two groups (4 warps each, one per TMEM lane
+    // quarter) take alternate tiles.  Software-pipelined: the SubnetNorm row
+    // and residual of the NEXT chunk (possibly of the group's next tile) are
+    // in flight while this chunk is drained.
     const int ew = warp - 1;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warps 1-4, 5-8)
     const int group = ew >> 2;     // tile parity this warp drains
     float* stg = epi_stage + ew * (32 * TC_STG_LD);
     const int seg = lane & 3, rsub = lane >> 2;
-    const float* scale = d.scale;
-    const float* shift = d.shift;
-    int i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      if ((i & 1) != group) continue;
-      const int a = i % NACC;
-      const uint32_t use = static_cast<uint32_t>(i / NACC);
+    const int nchunk = (bn + 31) / 32;
+    const bool sc_vec = ((reinterpret_cast<uintptr_t>(d.scale) | reinterpret_cast<uintptr_t>(d.shift)) & 15) == 0 &&
+                        (d.cout & 3) == 0;
+    auto chunks_of = [&](int t) {
+      const int left = d.cout - (t % nt) * bn;
+      return min(nchunk, (left + 31) / 32);
+    };
+    auto fetch = [&](EpiIn& in, int t, int c) {
       const int m0 = (t / nt) * TC_BM + quarter * 32;
-      const int n0 = (t % nt) * bn;
-      for (int cc = 0; cc < bn; cc += 32) {
-        if (n0 + cc >= d.cout) break;  // warp-uniform
-        // everything that does not depend on the accumulator is issued first
-        const int col = n0 + cc + seg * 8;
-        const bool colok = col < d.cout && cc + seg * 8 < bn;
-        // 8-wide vector path unless this is the ragged tail of a cout % 8 != 0
-        // slice (e.g. a 2-label classifier): then scalar loads and stores.
-        const int nv = colok ? min(8, d.cout - col) : 0;
-        const bool vec = EPI != 2 || (nv == 8 && (d.cout & 7) == 0);
-        float sc[8], sh[8];
-        uint4 rv[4];
-        if (colok) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int cq = EPI == 2 ? min(col + q, d.cout - 1) : col + q;  // ragged: clamp
-            sc[q] = scale ? __ldg(scale + cq) : 1.f;
-            sh[q] = shift ? __ldg(shift + cq) : 0.f;
-          }
-          if (p.res) {
-#pragma unroll
-            for (int r4 = 0; r4 < 4; ++r4) {
-              const int m = m0 + rsub + 8 * r4;
-              if (m >= p.M) continue;
-              const __nv_bfloat16* rp =
-                  static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col;
-              rv[r4] = vec ? __ldg(reinterpret_cast<const uint4*>(rp)) : load_ragged_bf16x8(rp, nv);
-            }
-          }
-        }
-        if (cc == 0) {
-          mbar_wait(&tfull[a], use & 1);
-          tc_fence_after();
-        }
-        float v[32];
-        tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
-        float4* srow = reinterpret_cast<float4*>(stg + lane * TC_STG_LD);
+      const int cc = c * 32;
+      const int col = (t % nt) * bn + cc + seg * 8;
+      const bool colok = col < d.cout && cc + seg * 8 < bn;
+      const int nv = colok ? min(8, d.cout - col) : 0;
+      const bool vec = EPI != 2 || (nv == 8 && (d.cout & 7) == 0);
+      if (!colok) return;
+      // EPI 0/1: SubnetNorm rows and biases are 16-byte aligned (engine
+      // tables; the operator API routes unaligned vectors to EPI 2)
+      const bool v4 = EPI != 2 || (sc_vec && nv == 8);
+      if (d.scale && v4) {
+        const float4 s0 = __ldg(reinterpret_cast<const float4*>(d.scale + col));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(d.scale + col + 4));
+        in.sc[0] = s0.x; in.sc[1] = s0.y; in.sc[2] = s0.z; in.sc[3] = s0.w;
+        in.sc[4] = s1.x; in.sc[5] = s1.y; in.sc[6] = s1.z; in.sc[7] = s1.w;
+      } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          srow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          in.sc[q] = d.scale ? __ldg(d.scale + (EPI == 2 ? min(col + q, d.cout - 1) : col + q)) : 1.f;
+      }
+      if (d.shift && v4) {
+        const float4 h0 = __ldg(reinterpret_cast<const float4*>(d.shift + col));
+        const float4 h1 = __ldg(reinterpret_cast<const float4*>(d.shift + col + 4));
+        in.sh[0] = h0.x; in.sh[1] = h0.y; in.sh[2] = h0.z; in.sh[3] = h0.w;
+        in.sh[4] = h1.x; in.sh[5] = h1.y; in.sh[6] = h1.z; in.sh[7] = h1.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          in.sh[q] = d.shift ? __ldg(d.shift + (EPI == 2 ? min(col + q, d.cout - 1) : col + q)) : 0.f;
+      }
+      if (p.res) {
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const int m = m0 + rsub + 8 * r4;
+          if (m >= p.M) continue;
+          const __nv_bfloat16* rp =
+              static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col;
+          in.rv[r4] = vec ? __ldg(reinterpret_cast<const uint4*>(rp)) : load_ragged_bf16x8(rp, nv);
+        }
+      }
+    };
+    int i = group;  // local tile ordinal
+    int t = blockIdx.x + i * static_cast<int>(gridDim.x);
+    int c = 0;
+    EpiIn cur, nxt;
+    if (t < tiles && !(p.dbg & 1)) fetch(cur, t, 0);
+    while (t < tiles) {
+      int tn = t, cn = c + 1, inx = i;
+      if (cn >= chunks_of(t)) {
+        cn = 0;
+        inx = i + 2;
+        tn = t + 2 * static_cast<int>(gridDim.x);
+      }
+      if (tn < tiles && !(p.dbg & 1)) fetch(nxt, tn, cn);
+      const int a = i % NACC;
+      if (c == 0) {
+        if (prof) {
+          const long long t0 = clock64();
+          mbar_wait(&tfull[a], static_cast<uint32_t>(i / NACC) & 1);
+          w_wait += clock64() - t0;
+        } else {
+          mbar_wait(&tfull[a], static_cast<uint32_t>(i / NACC) & 1);
+        }
+        tc_fence_after();
+      }
+      const int m0 = (t / nt) * TC_BM + quarter * 32;
+      const int cc = c * 32;
+      const int col = (t % nt) * bn + cc + seg * 8;
+      const bool colok = col < d.cout && cc + seg * 8 < bn;
+      const int nv = colok ? min(8, d.cout - col) : 0;
+      const bool vec = EPI != 2 || (nv == 8 && (d.cout & 7) == 0);
+      float v[32];
+      tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+      float4* srow = reinterpret_cast<float4*>(stg + lane * TC_STG_LD);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        srow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      __syncwarp();
+      if (cn == 0) {  // last chunk of this tile read out of TMEM: free the accumulator
+        tc_fence_before();
         __syncwarp();
-        if (colok) {
+        if (lane == 0) mbar_arrive(&tempty[a]);
+      }
+      if (colok && !(p.dbg & 1)) {
 #pragma unroll
-          for (int r4 = 0; r4 < 4; ++r4) {
-            const int rr = rsub + 8 * r4;
-            const int m = m0 + rr;
-            if (m >= p.M) continue;
-            const float4* sp = reinterpret_cast<const float4*>(stg + rr * TC_STG_LD + seg * 8);
-            const float4 lo = sp[0], hi = sp[1];
-            float o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const int rr = rsub + 8 * r4;
+          const int m = m0 + rr;
+          if (m >= p.M) continue;
+          const float4* sp = reinterpret_cast<const float4*>(stg + rr * TC_STG_LD + seg * 8);
+          const float4 lo = sp[0], hi = sp[1];
+          float o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = o[q] * sc[q] + sh[q];
-            float r8[8];
-            if (p.res) {
-              const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[r4]);
+          for (int q = 0; q < 8; ++q) o[q] = o[q] * cur.sc[q] + cur.sh[q];
+          float r8[8];
+          if (p.res) {
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&cur.rv[r4]);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float2 f = __bfloat1622float2(rh[q]);
-                r8[2 * q] = f.x;
-                r8[2 * q + 1] = f.y;
-              }
-              if (!p.res_post) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) o[q] += r8[q];
-              }
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __bfloat1622float2(rh[q]);
+              r8[2 * q] = f.x;
+              r8[2 * q + 1] = f.y;
             }
-            if (p.act == 1) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
-            } else if (EPI == 1 && p.act == 2) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] *= fminf(fmaxf(o[q] + 3.f, 0.f), 6.f) * (1.f / 6.f);
-            } else if (EPI == 2 && p.act) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] = act_apply(o[q], p.act);
-            }
-            if (p.res && p.res_post) {
+            if (!p.res_post) {
 #pragma unroll
               for (int q = 0; q < 8; ++q) o[q] += r8[q];
             }
-            const size_t off = static_cast<size_t>(m) * d.cout + col;
-            if (!vec) {
-              store_ragged8(p.y, off, nv, p.out_f32, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
-            } else if (p.out_f32) {
-              float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + off);
-              yp[0] = make_float4(o[0], o[1], o[2], o[3]);
-              yp[1] = make_float4(o[4], o[5], o[6], o[7]);
-            } else {
-              uint4 pk;
-              pk.x = pack_bf16x2(o[0], o[1]);
-              pk.y = pack_bf16x2(o[2], o[3]);
-              pk.z = pack_bf16x2(o[4], o[5]);
-              pk.w = pack_bf16x2(o[6], o[7]);
-              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + off) = pk;
-            }
+          }
+          if (p.act == 1) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
+          } else if (EPI == 1 && p.act == 2) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] *= fminf(fmaxf(o[q] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+          } else if (EPI == 2 && p.act) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = act_apply(o[q], p.act);
+          }
+          if (p.res && p.res_post) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] += r8[q];
+          }
+          const size_t off = static_cast<size_t>(m) * d.cout + col;
+          if (!vec) {
+            store_ragged8(p.y, off, nv, p.out_f32, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+          } else if (p.out_f32) {
+            float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + off);
+            yp[0] = make_float4(o[0], o[1], o[2], o[3]);
+            yp[1] = make_float4(o[4], o[5], o[6], o[7]);
+          } else {
+            uint4 pk;
+            pk.x = pack_bf16x2(o[0], o[1]);
+            pk.y = pack_bf16x2(o[2], o[3]);
+            pk.z = pack_bf16x2(o[4], o[5]);
+            pk.w = pack_bf16x2(o[6], o[7]);
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + off) = pk;
           }
         }
-        __syncwarp();  // staging tile is rewritten by the next chunk
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
+      __syncwarp();  // staging tile is rewritten by the next chunk
+      cur = nxt;
+      t = tn;
+      c = cn;
+      i = inx;
     }
   } else {
     // ============================================================ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc_bf16(bn);
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      int g = 0, i = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-        const int a = i % NACC;
-        const uint32_t use = static_cast<uint32_t>(i / NACC);
+    const bool leader = elect_one();
+    const uint32_t idesc = umma_idesc_bf16(bn);
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    int g = 0, i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int a = i % NACC;
+      const uint32_t use = static_cast<uint32_t>(i / NACC);
+      if (prof) {
+        const long long t0 = clock64();
         mbar_wait(&tempty[a], (use & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t acc = tmem + a * BN_MAX;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % STAGES;
-          const uint32_t ph = (g / STAGES) & 1;
+        w_wait2 += clock64() - t0;
+      } else {
+        mbar_wait(&tempty[a], (use & 1) ^ 1);
+      }
+      tc_fence_after();
+      const uint32_t acc = tmem + a * BN_MAX;
+      for (int kb = 0; kb < nk; kb += KPS, ++g) {
+        const int s = g % STAGES;
+        const uint32_t ph = (g / STAGES) & 1;
+        if (prof) {
+          const long long t0 = clock64();
           mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(a0 + s * C::A_BYTES);
-          const uint64_t bd = umma_desc_sw128(b0 + s * C::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk)
-            tc_mma_bf16(acc, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2),
-                        idesc, (kb | kk) != 0 ? 1u : 0u);
-          tc_commit(&empty[s]);
+          w_wait += clock64() - t0;
+        } else {
+          mbar_wait(&full[s], ph);
         }
-        tc_commit(&tfull[a]);
+        tc_fence_after();
+        const int nsub = min(KPS, nk - kb);
+        if (leader) {
+#pragma unroll
+          for (int j = 0; j < KPS; ++j) {
+            if (j < nsub) {
+              const uint64_t ad = umma_desc_sw128(a0 + (s * KPS + j) * C::A_BYTES);
+              const uint64_t bd = umma_desc_sw128(b0 + (s * KPS + j) * C::B_BYTES);
+#pragma unroll
+              for (int kk = 0; kk < TC_BK / 16; ++kk)
+                if (!(p.dbg & 2))
+                  tc_mma_bf16(acc, ad + static_cast<uint64_t>(kk * 2),
+                              bd + static_cast<uint64_t>(kk * 2), idesc,
+                              ((kb + j) | kk) != 0 ? 1u : 0u);
+            }
+          }
+          tc_commit(&empty[s]);
+          if (kb + KPS >= nk) tc_commit(&tfull[a]);
+        }
+        __syncwarp();
       }
     }
-    __syncwarp();
   }
+  if (prof && lane == 0 && (warp == TC_PROD_WARP || warp == TC_MMA_WARP || warp == 1))
+    printf("[conv_tc prof] tiles=%d nk=%d warp=%d total=%lld wait=%lld wait2=%lld\n", tiles, nk, warp,
+           clock64() - t_begin, w_wait, w_wait2);
   tc_fence_before();
   __syncthreads();
   if (warp == TC_MMA_WARP) {
@@ -421,44 +541,51 @@ int choose_bn(int cout_max, long M) {
   return cost(128) < cost(256) ? 128 : 256;
 }
 
-// Instances: ring depth chosen so operands + epilogue staging fit 227 KB.
-#define SSN_TC_INSTANCES(X) X(64, 7) X(128, 5) X(256, 3)
+// Instances (BN_MAX, STAGES, K blocks per stage): the operand ring plus the
+// 36 KB epilogue staging fill the 227 KB of shared memory.
+#define SSN_TC_INSTANCES(X) X(64, 7, 1) X(128, 5, 1) X(256, 3, 1)
 
 cudaError_t init_conv_tc() {
-#define SSN_TC_ATTR(BN, ST)                                                             \
-  {                                                                                     \
-    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, 0>,               \
-                                               conv_tc_kernel<BN, ST, 1>,               \
-                                               conv_tc_kernel<BN, ST, 2>};              \
-    for (auto fn : fns) {                                                               \
+#define SSN_TC_ATTR(BN, ST, KPS)                                                          \
+  {                                                                                       \
+    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, KPS, 0>,            \
+                                               conv_tc_kernel<BN, ST, KPS, 1>,            \
+                                               conv_tc_kernel<BN, ST, KPS, 2>};           \
+    for (auto fn : fns) {                                                                 \
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           TcCfg<BN, ST>::SMEM);                        \
-      if (e != cudaSuccess) return e;                                                   \
-    }                                                                                   \
+                                           TcCfg<BN, ST, KPS>::SMEM);                     \
+      if (e != cudaSuccess) return e;                                                     \
+    }                                                                                     \
   }
   SSN_TC_INSTANCES(SSN_TC_ATTR)
 #undef SSN_TC_ATTR
   return cudaSuccess;
 }
 
-template <int BN_MAX, int STAGES>
+template <int BN_MAX, int STAGES, int KPS>
 static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
-  using C = TcCfg<BN_MAX, STAGES>;
+  using C = TcCfg<BN_MAX, STAGES, KPS>;
   const long tiles = static_cast<long>((p.M + TC_BM - 1) / TC_BM) * ((p.cout_max + p.bn - 1) / p.bn);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   if (p.act > 2 || (p.cout_max & 7) != 0 || p.ragged)
-    conv_tc_kernel<BN_MAX, STAGES, 2><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    conv_tc_kernel<BN_MAX, STAGES, KPS, 2><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   else if (p.act == 2)
-    conv_tc_kernel<BN_MAX, STAGES, 1><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    conv_tc_kernel<BN_MAX, STAGES, KPS, 1><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   else
-    conv_tc_kernel<BN_MAX, STAGES, 0><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    conv_tc_kernel<BN_MAX, STAGES, KPS, 0><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
-  if (p.bn <= 64) return launch_impl<64, 7>(p, wmap, s);
-  if (p.bn <= 128) return launch_impl<128, 5>(p, wmap, s);
-  return launch_impl<256, 3>(p, wmap, s);
+cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s) {
+  static const int dbg = [] {
+    const char* e = getenv("SSN_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  ConvParams p = p_in;
+  p.dbg = dbg;
+  if (p.bn <= 64) return launch_impl<64, 7, 1>(p, wmap, s);
+  if (p.bn <= 128) return launch_impl<128, 5, 1>(p, wmap, s);
+  return launch_impl<256, 3, 1>(p, wmap, s);
 }
 
 }  // namespace ssn

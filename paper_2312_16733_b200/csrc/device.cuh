@@ -110,6 +110,8 @@ struct ConvParams {
   int act, res_post, out_f32, depthwise;
   int bn;             // N tile (tcgen05 path)
   int ragged;         // some active cout may be % 8 != 0 (scalar epilogue tail)
+  int dbg;            // profiling knob (SSN_TC_DEBUG): 1 = epilogue skips global
+                      // memory, 2 = no MMA issued (bottleneck isolation only)
 };
 
 

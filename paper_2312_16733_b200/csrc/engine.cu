@@ -991,7 +991,8 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.res_post = 0;
     p.out_f32 = out_f32;
     p.bn = choose_bn(cout_max, p.M);
-    p.ragged = (cout & 7) != 0;
+    // ragged slice, or SubnetNorm vectors the vector epilogue cannot load
+    p.ragged = (cout & 7) != 0 || ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) != 0;
     CUtensorMap wmap{};
     if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
