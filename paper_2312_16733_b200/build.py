@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libssn.so")
-SOURCES = ["engine.cu", "conv_tc.cu", "kernels.cu", "transformer.cu"]
+SOURCES = ["engine.cu", "conv_tc.cu", "conv_halo.cu", "kernels.cu", "transformer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,393 @@
+// conv_halo.cu — stride-1 k x k WeightSlice convolution as a "shifted-window"
+// implicit GEMM on tcgen05 (sm_100a), for the narrow early layers of the
+// CNN supernets (OFA-ResNet50 stem and stage-1 3x3 convs: 24-88 channels at
+// 56-112 px).
+//
+// Why a second conv kernel: with TMA im2col every K block of
+// conv_tc re-reads the 128-pixel A tile per filter tap, 9x for a 3x3, and a
+// narrow N (cout <= 96) gives the tensor core only ~200 cycles of work per
+// 28 KB K block.  The ring then cannot hold enough bytes to cover the TMA
+// latency (measured: MMA warp waiting on data 67% of the time; 0.07-0.17 of
+// roofline on these layers).  Here:
+//  * the whole active weight slice (k_a^2 x cin_a x cout_a, <= ~160 KB) is
+//    loaded into shared memory ONCE per CTA and stays resident;
+//  * output positions are taken in padded-width order (HaloGeom): tap (r, s)
+//    of position p reads window pixel p + r*Wp + s, so ONE halo window per
+//    32-channel block feeds all k^2 taps — each tap's A operand is the same
+//    smem window at a row offset.  That needs the no-swizzle K-major UMMA
+//    layout ([8-channel chunk][pixel][8] — 16-byte rows, any 16-byte offset
+//    is a valid descriptor start), which a 5-D TMA box {8 ch, Wp, R, 1, 4
+//    chunks} over the NHWC activation produces directly (the channel-chunk
+//    dimension has a 16-byte global stride and is outermost in the box);
+//  * A traffic drops from 9 x 128 to ~(R x Wp) pixels per tile, and the
+//    padding columns/rows are TMA zero fill.
+// Garbage positions (the k-1 padding columns of each row, rows past H) are
+// computed and dropped by the epilogue (3.4% of MMA work at 56 px).
+// Warp roles as conv_tc: warp 0 TMA producer, warp 9 MMA issuer (one
+// elected lane), warps 1-8 epilogue in two groups of 4 taking alternate
+// tiles; accumulators in a TMEM ring.  The epilogue is row-per-lane (no
+// smem staging: shared memory belongs to the resident weights).
+#include <cstdio>
+#include <cstdlib>
+
+#include "device.cuh"
+
+namespace ssn {
+
+constexpr int HL_EPI_WARPS = 8;
+constexpr int HL_MMA_WARP = 1 + HL_EPI_WARPS;
+constexpr int HL_THREADS = (HL_MMA_WARP + 1) * 32;
+constexpr int HL_SMEM_MAX = 232448;  // 227 KB opt-in
+constexpr int HL_CB = 32;            // channels per A stage (two K=16 steps)
+
+__global__ void __launch_bounds__(HL_THREADS, 1)
+    conv_halo_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+
+  const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
+  const OpDims d = load_desc(p.row, p.fixed, p.op);
+  const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
+  const HaloGeom hg = halo_geom(p.w_, ka);
+  const int wp = hg.wp, rt = hg.rt, R = hg.r;
+  const int tpi = (p.h + rt - 1) / rt;  // tiles per image
+  const int tiles = p.n * tpi;
+  if (static_cast<int>(blockIdx.x) >= tiles) return;
+  const int cin16 = (d.cin + 15) & ~15;
+  const int ncb = (cin16 + HL_CB - 1) / HL_CB;
+  const int bn = (d.cout + 15) & ~15;  // MMA N: the whole active cout (<= 256)
+  const int acc_cols = bn <= 128 ? 128 : 256;
+  const int nacc = 512 / acc_cols > 4 ? 4 : 512 / acc_cols;
+
+  // shared memory: [resident B][A ring][barriers]
+  const uint32_t b_chunk = static_cast<uint32_t>(p.hb_rows) * 16;      // K-chunk stride in B
+  const uint32_t b_tap = b_chunk * static_cast<uint32_t>(p.hb_chunks);  // tap stride in B
+  const uint32_t b_bytes = b_tap * static_cast<uint32_t>(ka * ka);
+  const uint32_t a_chunk = static_cast<uint32_t>(R * wp) * 16;         // K-chunk stride in A
+  const uint32_t a_stage = (a_chunk * (HL_CB / 8) + 127) & ~127u;  // TMA dst: 128-B aligned
+  const int ST = p.h_stages;
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + ((b_bytes + 1023) & ~1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + ST * a_stage);
+  uint64_t* full = bars;
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;    // [4]
+  uint64_t* tempty = tfull + 4;    // [4]
+  uint64_t* bfull = tempty + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 4; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], HL_EPI_WARPS / 2);
+    }
+    mbar_init(bfull, 1);
+    fence_mbar_init();
+    tma_prefetch(&wmap);
+    tma_prefetch(&dp->amap);
+  }
+  if (warp == HL_MMA_WARP) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================================================ producer
+    const bool leader = elect_one();
+    if (leader) {
+      // the active k_a x k_a centre crop of the max-shape weights, all cin/cout
+      // chunks of the max shape (channels past cin_a meet zero-filled A)
+      mbar_arrive_expect_tx(bfull, b_bytes);
+      for (int r = 0; r < ka; ++r)
+        for (int s = 0; s < ka; ++s)
+          tma_load_4d(sB + (r * ka + s) * b_tap, &wmap, bfull, 0, 0, 0,
+                      (r + koff) * p.k_max + (s + koff));
+    }
+    const CUtensorMap* amap = &dp->amap;
+    int g = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int img = t / tpi;
+      const int r0 = (t - img * tpi) * rt;
+      for (int cb = 0; cb < ncb; ++cb, ++g) {
+        const int s = g % ST;
+        mbar_wait(&empty[s], ((g / ST) & 1) ^ 1);
+        if (leader) {
+          mbar_arrive_expect_tx(&full[s], a_chunk * (HL_CB / 8));  // box bytes (stage is padded)
+          tma_load_5d(sA + s * a_stage, amap, &full[s], 0, -pad, r0 - pad, img, cb * (HL_CB / 8));
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == HL_MMA_WARP) {
+    // ============================================================ MMA issuer
+    const bool leader = elect_one();
+    const uint32_t idesc = umma_idesc_bf16(bn);
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    mbar_wait(bfull, 0);
+    tc_fence_after();
+    int g = 0, i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int a = i % nacc;
+      mbar_wait(&tempty[a], ((i / nacc) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + a * acc_cols;
+      for (int cb = 0; cb < ncb; ++cb, ++g) {
+        const int s = g % ST;
+        mbar_wait(&full[s], (g / ST) & 1);
+        tc_fence_after();
+        const int nks = min(HL_CB / 16, (cin16 - cb * HL_CB) / 16);
+        if (leader) {
+          for (int r = 0; r < ka; ++r)
+            for (int c = 0; c < ka; ++c) {
+              const uint32_t a_tap = a0 + s * a_stage + static_cast<uint32_t>(r * wp + c) * 16;
+              const uint32_t b_at = b0 + (r * ka + c) * b_tap + cb * (HL_CB / 8) * b_chunk;
+              for (int j = 0; j < nks; ++j)
+                tc_mma_bf16(acc, umma_desc_noswz(a_tap + 2 * j * a_chunk, a_chunk, 128),
+                            umma_desc_noswz(b_at + 2 * j * b_chunk, b_chunk, 128), idesc,
+                            (cb | r | c | j) != 0 ? 1u : 0u);
+            }
+          tc_commit(&empty[s]);
+          if (cb + 1 == ncb) tc_commit(&tfull[a]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ============================================================ epilogue
+    // Lane L of warp w drains TMEM row 32*(w%4) + L = one padded output
+    // position; positions in the padding columns / past H are dropped.
+    const int quarter = warp & 3;
+    const int group = (warp - 1) >> 2;
+    const int p_row = quarter * 32 + lane;
+    const int oh_l = p_row / wp, ow = p_row - oh_l * wp;
+    const int nch = (d.cout + 31) / 32;
+    int i = group;
+    for (int t = blockIdx.x + group * static_cast<int>(gridDim.x); t < tiles;
+         t += 2 * static_cast<int>(gridDim.x), i += 2) {
+      const int a = i % nacc;
+      const int img = t / tpi;
+      const int oh = (t - img * tpi) * rt + oh_l;
+      const bool ok = p_row < rt * wp && ow < p.wo && oh < p.ho;
+      const size_t m = (static_cast<size_t>(img) * p.ho + oh) * p.wo + ow;
+      const size_t rowoff = m * d.cout;
+      mbar_wait(&tfull[a], static_cast<uint32_t>(i / nacc) & 1);
+      tc_fence_after();
+      for (int c = 0; c < nch; ++c) {
+        float v[32];
+        tmem_ld32(tmem + a * acc_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+        if (c + 1 == nch) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[a]);
+        }
+        if (!ok) continue;
+        uint4 rv[4];
+        if (p.res) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (c * 32 + 8 * j < d.cout)
+              rv[j] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.res) +
+                                                           rowoff + c * 32 + 8 * j));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = c * 32 + 8 * j;
+          if (col >= d.cout) break;
+          float sc[8], sh[8];
+          if (d.scale) {
+            const float4 s0 = __ldg(reinterpret_cast<const float4*>(d.scale + col));
+            const float4 s1 = __ldg(reinterpret_cast<const float4*>(d.scale + col + 4));
+            sc[0] = s0.x; sc[1] = s0.y; sc[2] = s0.z; sc[3] = s0.w;
+            sc[4] = s1.x; sc[5] = s1.y; sc[6] = s1.z; sc[7] = s1.w;
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sc[q] = 1.f;
+          }
+          if (d.shift) {
+            const float4 h0 = __ldg(reinterpret_cast<const float4*>(d.shift + col));
+            const float4 h1 = __ldg(reinterpret_cast<const float4*>(d.shift + col + 4));
+            sh[0] = h0.x; sh[1] = h0.y; sh[2] = h0.z; sh[3] = h0.w;
+            sh[4] = h1.x; sh[5] = h1.y; sh[6] = h1.z; sh[7] = h1.w;
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sh[q] = 0.f;
+          }
+          float o[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o[q] = v[8 * j + q] * sc[q] + sh[q];
+          float r8[8];
+          if (p.res) {
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[j]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __bfloat1622float2(rh[q]);
+              r8[2 * q] = f.x;
+              r8[2 * q + 1] = f.y;
+            }
+            if (!p.res_post) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] += r8[q];
+            }
+          }
+          if (p.act == 1) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
+          }
+          if (p.res && p.res_post) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] += r8[q];
+          }
+          uint4 pk;
+          pk.x = pack_bf16x2(o[0], o[1]);
+          pk.y = pack_bf16x2(o[2], o[3]);
+          pk.z = pack_bf16x2(o[4], o[5]);
+          pk.w = pack_bf16x2(o[6], o[7]);
+          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + rowoff + col) = pk;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == HL_MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+using EncodeTiledFnH = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFnH tiled_encoder() {
+  static EncodeTiledFnH fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<EncodeTiledFnH>(ptr);
+    return static_cast<EncodeTiledFnH>(nullptr);
+  }();
+  return fn;
+}
+
+static int halo_b_rows(int cout_max) { return (cout_max + 15) / 16 * 16; }
+static int halo_b_chunks(int cin_max) { return (cin_max + 15) / 16 * 2; }
+
+// Resident-B and ring sizing for an op's MAX shape (every subnet fits in it).
+static void halo_sizes(int w, int k_max, int cin_max, int cout_max, long* b_bytes, long* a_stage) {
+  const HaloGeom g = halo_geom(w, k_max);
+  *b_bytes = static_cast<long>(k_max) * k_max * halo_b_chunks(cin_max) * halo_b_rows(cout_max) * 16;
+  *a_stage = (static_cast<long>(g.r) * g.wp * 16 * (HL_CB / 8) + 127) & ~127L;
+}
+
+static int halo_stages(int w, int k_max, int cin_max, int cout_max) {
+  long bb, as;
+  halo_sizes(w, k_max, cin_max, cout_max, &bb, &as);
+  const long avail = HL_SMEM_MAX - 1024 - ((bb + 1023) & ~1023L) - 256;
+  const long st = avail / as;
+  return static_cast<int>(st > 6 ? 6 : st);
+}
+
+// The shifted-window kernel serves stride-1 odd k x k convs whose max-shape
+// weight slice fits shared memory with >= 2 ring stages, cout <= 256.
+bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max) {
+  static const bool off = [] {
+    const char* e = getenv("SSN_NO_HALO");  // A/B switch for profiling
+    return e && atoi(e) != 0;
+  }();
+  if (off) return false;
+  if (stride != 1 || (k_max & 1) == 0 || k_max < 3 || cout_max > 256) return false;
+  if (w < 14 || h < 2) return false;
+  const HaloGeom g = halo_geom(w, k_max);
+  if (g.wp > 256 || g.r > 256) return false;
+  return halo_stages(w, k_max, cin_max, cout_max) >= 2;
+}
+
+// A operand: [n][h][w][cin] NHWC bf16 viewed as (c8, w, h, n, c/8) so the box
+// {8, Wp, R, 1, 4} lands as [chunk][row][col][8]: 4 K-chunks of the halo
+// window, pixel rows 16 bytes apart (no-swizzle K-major core matrices).
+int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k) {
+  EncodeTiledFnH enc = tiled_encoder();
+  if (!enc) return -1;
+  const HaloGeom g = halo_geom(w, k);
+  cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                        static_cast<cuuint64_t>(n), static_cast<cuuint64_t>((cin + 7) / 8)};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(w) * cin * 2,
+                           static_cast<cuuint64_t>(h) * w * cin * 2, 16};
+  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(g.wp), static_cast<cuuint32_t>(g.r), 1,
+                       HL_CB / 8};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
+}
+
+// B operand: max-shape KRSC [cout][taps][cin_store] viewed as (c8, n, c/8, tap);
+// one box {8, rows, chunks, 1} per tap lands as [chunk][n][8].
+static int make_halo_weight_map(CUtensorMap* map, const void* wgt, int cin_store, int taps,
+                                int cout, int rows, int chunks) {
+  EncodeTiledFnH enc = tiled_encoder();
+  if (!enc) return -1;
+  cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(cout),
+                        static_cast<cuuint64_t>((cin_store + 7) / 8), static_cast<cuuint64_t>(taps)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(taps) * cin_store * 2, 16,
+                           static_cast<cuuint64_t>(cin_store) * 2};
+  cuuint32_t box[4] = {8, static_cast<cuuint32_t>(rows), static_cast<cuuint32_t>(chunks), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(wgt), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+cudaError_t init_conv_halo() {
+  return cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              HL_SMEM_MAX);
+}
+
+// p: geometry of the op's max shape (k_max, cin_max = weight cin_store,
+// cout_max); the active subnet's extents and A map come from its OpDesc.
+cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps,
+                             cudaStream_t s) {
+  p.hb_rows = halo_b_rows(p.cout_max);
+  p.hb_chunks = halo_b_chunks(p.cin_max);
+  p.h_stages = halo_stages(p.w_, p.k_max, p.cin_max, p.cout_max);
+  if (p.h_stages < 2) return cudaErrorInvalidValue;
+  CUtensorMap wmap;
+  if (make_halo_weight_map(&wmap, wgt, cin_store, taps, p.cout_max, p.hb_rows, p.hb_chunks) != 0)
+    return cudaErrorInvalidValue;
+  long bb, as;
+  halo_sizes(p.w_, p.k_max, p.cin_max, p.cout_max, &bb, &as);
+  const long smem = 1024 + ((bb + 1023) & ~1023L) + p.h_stages * as + (2 * p.h_stages + 9) * 8 + 16;
+  const HaloGeom g = halo_geom(p.w_, p.k_max);
+  const long tiles = static_cast<long>(p.n) * ((p.h + g.rt - 1) / g.rt);
+  const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
+  conv_halo_kernel<<<grid, HL_THREADS, smem, s>>>(p, wmap);
+  return cudaGetLastError();
+}
+
+}  // namespace ssn

@@ -63,13 +63,6 @@ struct TcCfg {
   static_assert(SMEM <= 232448, "operand ring exceeds 227 KB of shared memory");
 };
 
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
-      : "=r"(pred));
-  return pred != 0;
-}
 
 // Ragged tail of a cout % 8 != 0 slice (e.g. a 2-label classifier): scalar
 // accesses, kept out of line so the 8-wide vector epilogue stays compact.

@@ -110,10 +110,29 @@ struct ConvParams {
   int act, res_post, out_f32, depthwise;
   int bn;             // N tile (tcgen05 path)
   int ragged;         // some active cout may be % 8 != 0 (scalar epilogue tail)
+  // halo kernel (conv_halo.cu): resident weight box rows / K chunks, A ring depth
+  int hb_rows, hb_chunks, h_stages;
   int dbg;            // profiling knob (SSN_TC_DEBUG): 1 = epilogue skips global
                       // memory, 2 = no MMA issued (bottleneck isolation only)
 };
 
+
+// Halo ("shifted-window") geometry of a stride-1 k x k conv over a W-wide
+// image: output positions are taken in PADDED-width row-major order (Wp =
+// W + k - 1 columns, k - 1 of them garbage), so tap (r, s) of position p reads
+// padded input pixel p + r*Wp + s: a plain row offset into ONE smem window.
+// A tile is RT whole padded rows (<= 128 positions); its window is R rows,
+// enough that all 128 MMA rows of every tap stay inside the window.
+struct HaloGeom {
+  int wp, rt, r;
+};
+__host__ __device__ __forceinline__ HaloGeom halo_geom(int w, int k) {
+  HaloGeom g;
+  g.wp = w + k - 1;
+  g.rt = g.wp >= 128 ? 1 : 128 / g.wp;
+  g.r = (128 + (k - 1) * (g.wp + 1) + g.wp - 1) / g.wp;
+  return g;
+}
 
 struct PoolParams {
   const void* x;
@@ -177,10 +196,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Bounded: a pipeline bug (e.g. an expect_tx byte count that the TMA never
+// delivers) traps after ~2^30 polls (tens of seconds) instead of hanging the
+// GPU until the process is killed.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
+  uint32_t spins = 0;
   do {
+    if (++spins == (1u << 30)) __trap();
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -222,6 +246,25 @@ __device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* map,
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
       "h"(off_w), "h"(off_h)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3), "r"(c4)
+      : "memory");
+}
+
+// One lane of a converged warp (elect.sync): keeps the issue loop warp-uniform.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {

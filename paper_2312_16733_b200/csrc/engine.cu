@@ -36,6 +36,10 @@ int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, 
 int choose_bn(int cout_max, long M);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
+cudaError_t init_conv_halo();
+bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max);
+int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k);
+cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps, cudaStream_t s);
 cudaError_t launch_input(const InputParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
@@ -222,6 +226,17 @@ static void* slot_ptr(ssn_engine* e, int slot, const int* map) {
 }
 
 // Enqueue one op (called under stream capture).
+// Narrow stride-1 3x3 convs (OFA-R50 stem and stage 1) run the shifted-window
+// kernel with resident weights (conv_halo.cu); the choice depends only on the
+// op's max shape, so one graph serves every subnet.
+static bool use_halo(const ssn_engine* e, const OpSpec& o) {
+  if (!e->bf16 || o.kind != OP_CONV || o.depthwise || o.act > 1 || (o.cout_max & 7) != 0)
+    return false;
+  const TensorSpec& t = e->net.tensors[o.tensor];
+  if (t.im2col_stem) return false;
+  return halo_eligible(o.hin, o.win, o.k_max, o.stride, t.cin_store, o.cout_max);
+}
+
 static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cudaStream_t s) {
   const OpSpec& o = e->net.ops[oi];
   const bool bf = e->bf16;
@@ -290,7 +305,9 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.res_post = o.res_post;
       p.out_f32 = o.kind == OP_LINEAR;
       p.depthwise = o.depthwise;
-      if (bf && !o.depthwise) {
+      if (bf && use_halo(e, o)) {
+        CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
+      } else if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M);
         CUtensorMap wmap{};
         if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
@@ -524,9 +541,15 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     if (e->bf16 && o.active && (o.kind == OP_CONV || o.kind == OP_LINEAR) && !o.depthwise) {
       // WeightSlice A operand: im2col TMA map over this subnet's compact
       // activation (cin_a channels) in the buffer its graph variant reads.
-      if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin, o.win,
-                       o.cin, o.k, o.stride, o.k / 2) != 0)
+      // Shifted-window (halo) convs read a 5-D tiled map instead.
+      if (use_halo(e, o)) {
+        if (make_halo_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
+                              o.win, o.cin, o.k) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (halo) failed for op " + std::to_string(oi));
+      } else if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
+                              o.win, o.cin, o.k, o.stride, o.k / 2) != 0) {
         SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed for op " + std::to_string(oi));
+      }
     }
     dsc.cin = o.cin;
     dsc.cout = o.cout;
@@ -645,7 +668,10 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
     if (e->bf16 && major != 10)
       SSN_THROW(SSN_E_CUDA, "bf16 tcgen05 path requires an sm_100 (B200) device");
-    if (e->bf16) CUDA_TRY(init_conv_tc());
+    if (e->bf16) {
+      CUDA_TRY(init_conv_tc());
+      CUDA_TRY(init_conv_halo());
+    }
     std::vector<uint8_t> gen;
     const uint8_t* blob = static_cast<const uint8_t*>(host_weights);
     if (!blob) {
@@ -967,9 +993,16 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     if (k < 1 || stride < 1 || pad < 0) SSN_THROW(SSN_E_INVALID, "bad geometry");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(init_conv_tc());
+    CUDA_TRY(init_conv_halo());
+    const bool aligned16 =
+        ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) == 0;
+    const bool halo = pad == k / 2 && !out_f32 && act <= 1 && (cout & 7) == 0 &&
+                      (cout_max & 7) == 0 && aligned16 &&
+                      halo_eligible(h, w, k, stride, cin_max, cout_max);
     OpDesc d = plain_desc(cin, cout, k, pad, scale, shift);
-    if (make_act_map(&d.amap, x, n, h, w, cin, k, stride, pad) != 0)
-      SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed");
+    if (halo ? make_halo_act_map(&d.amap, x, n, h, w, cin, k) != 0
+             : make_act_map(&d.amap, x, n, h, w, cin, k, stride, pad) != 0)
+      SSN_THROW(SSN_E_CUDA, "cuTensorMapEncode (activation) failed");
     ConvParams p{};
     p.x = x;
     p.y = y;
@@ -990,6 +1023,10 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.act = act;
     p.res_post = 0;
     p.out_f32 = out_f32;
+    if (halo) {
+      CUDA_TRY(launch_conv_halo(p, wgt, cin_max, k * k, s));
+      return;
+    }
     p.bn = choose_bn(cout_max, p.M);
     // ragged slice, or SubnetNorm vectors the vector epilogue cannot load
     p.ragged = (cout & 7) != 0 || ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) != 0;

@@ -74,6 +74,13 @@ CASES = [
     (64, 28, 28, 128, 128, 128, 128, 1, 1),
     (8, 14, 14, 256, 256, 1024, 1024, 1, 1),
     (16, 14, 14, 104, 128, 360, 360, 3, 1),
+    # shifted-window (halo) kernel: stride-1 3x3 with resident weights
+    (2, 56, 56, 88, 88, 88, 88, 3, 1),      # OFA-R50 stage-1 max
+    (2, 56, 56, 56, 88, 56, 88, 3, 1),      # WeightSlice of the max tensor
+    (1, 112, 112, 24, 32, 40, 64, 3, 1),    # stem 112 px (one window row-tile per row)
+    (3, 28, 28, 40, 64, 48, 64, 3, 1),      # cin16 = 48: a half channel block
+    (2, 20, 30, 16, 16, 16, 16, 3, 1),      # h != w, 4 rows per tile
+    (5, 17, 19, 32, 32, 64, 64, 3, 1),      # odd sizes, last tile past H
 ]
 
 
@@ -83,6 +90,12 @@ def test_conv_bf16_matches_oracle(gpu, case):
     got, ref = _run_bf16(gpu, n, h, w, cin, cin_max, cout, cout_max, k, stride)
     err = np.abs(got - ref).max() / (np.abs(ref).max() + 1e-6)
     assert err < 1e-2, f"max rel err {err}"
+
+
+def test_conv_bf16_halo_residual(gpu):
+    """The stem residual block (y + relu(bn(conv3x3(y)))) on the halo kernel."""
+    got, ref = _run_bf16(gpu, 2, 56, 56, 32, 32, 32, 32, 3, 1, res=True, act=1)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-2
 
 
 def test_conv_bf16_residual_and_f32_out(gpu):
