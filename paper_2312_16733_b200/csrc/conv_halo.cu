@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   uint64_t* bfull = tempty + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp index through shfl: the compiler then knows it is warp-uniform, so
+  // role branches stay uniform and MMA/TMA operands live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
@@ -96,11 +99,25 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
+  const bool prof = (p.dbg & 32) && blockIdx.x == 0;
+  long long w_wait = 0, w_wait2 = 0;
+  const long long t_begin = prof ? clock64() : 0;
+#define HL_WAIT(acc, bar, ph)                 \
+  if (prof) {                                 \
+    const long long t0_ = clock64();          \
+    mbar_wait(bar, ph);                       \
+    acc += clock64() - t0_;                   \
+  } else {                                    \
+    mbar_wait(bar, ph);                       \
+  }
 
   if (warp == 0) {
     // ============================================================ producer
     const bool leader = elect_one();
-    if (leader) {
+    if (leader && (p.dbg & 8)) {  // profiling: no weight load
+      mbar_arrive(bfull);
+    } else if (leader) {
       // the active k_a x k_a centre crop of the max-shape weights, all cin/cout
       // chunks of the max shape (channels past cin_a meet zero-filled A)
       mbar_arrive_expect_tx(bfull, b_bytes);
@@ -116,45 +133,63 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
       const int r0 = (t - img * tpi) * rt;
       for (int cb = 0; cb < ncb; ++cb, ++g) {
         const int s = g % ST;
-        mbar_wait(&empty[s], ((g / ST) & 1) ^ 1);
+        HL_WAIT(w_wait, &empty[s], ((g / ST) & 1) ^ 1);
         if (leader) {
-          mbar_arrive_expect_tx(&full[s], a_chunk * (HL_CB / 8));  // box bytes (stage is padded)
-          tma_load_5d(sA + s * a_stage, amap, &full[s], 0, -pad, r0 - pad, img, cb * (HL_CB / 8));
+          if (p.dbg & 4) {  // profiling: no A loads
+            mbar_arrive(&full[s]);
+          } else {
+            mbar_arrive_expect_tx(&full[s], a_chunk * (HL_CB / 8));  // box bytes (stage is padded)
+            tma_load_5d(sA + s * a_stage, amap, &full[s], 0, -pad, r0 - pad, img, cb * (HL_CB / 8));
+          }
         }
         __syncwarp();
       }
     }
   } else if (warp == HL_MMA_WARP) {
     // ============================================================ MMA issuer
-    const bool leader = elect_one();
+    // Converged warp, elected lane issues (tc_mma_bf16_elect); descriptors
+    // are a per-stage / per-block base plus 16-byte-unit offsets.
     const uint32_t idesc = umma_idesc_bf16(bn);
-    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-    mbar_wait(bfull, 0);
+    const uint64_t a_base = umma_desc_noswz(smem_u32(sA), a_chunk, 128);
+    const uint64_t b_base = umma_desc_noswz(smem_u32(sB), b_chunk, 128);
+    const uint32_t a_st16 = a_stage >> 4, a_ks16 = (2 * a_chunk) >> 4;
+    const uint32_t b_tap16 = b_tap >> 4, b_ks16 = (2 * b_chunk) >> 4, b_cb16 = ((HL_CB / 8) * b_chunk) >> 4;
+    HL_WAIT(w_wait, bfull, 0);
     tc_fence_after();
     int g = 0, i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int a = i % nacc;
-      mbar_wait(&tempty[a], ((i / nacc) & 1) ^ 1);
+      HL_WAIT(w_wait2, &tempty[a], ((i / nacc) & 1) ^ 1);
       tc_fence_after();
       const uint32_t acc = tmem + a * acc_cols;
       for (int cb = 0; cb < ncb; ++cb, ++g) {
         const int s = g % ST;
-        mbar_wait(&full[s], (g / ST) & 1);
+        HL_WAIT(w_wait, &full[s], (g / ST) & 1);
         tc_fence_after();
         const int nks = min(HL_CB / 16, (cin16 - cb * HL_CB) / 16);
-        if (leader) {
+        const uint64_t ad = a_base + static_cast<uint64_t>(s * a_st16);
+        const uint64_t bd = b_base + static_cast<uint64_t>(cb * b_cb16);
+        if (p.dbg & 2) {  // profiling: no MMAs
+        } else if (ka == 3 && nks == 2) {  // OFA-R50: fully unrolled 3x3 taps, full block
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(r * wp + c + j * a_ks16),
+                                  bd + static_cast<uint64_t>((r * 3 + c) * b_tap16 + j * b_ks16),
+                                  idesc, (cb | r | c | j) != 0 ? 1u : 0u);
+        } else {
           for (int r = 0; r < ka; ++r)
-            for (int c = 0; c < ka; ++c) {
-              const uint32_t a_tap = a0 + s * a_stage + static_cast<uint32_t>(r * wp + c) * 16;
-              const uint32_t b_at = b0 + (r * ka + c) * b_tap + cb * (HL_CB / 8) * b_chunk;
+            for (int c = 0; c < ka; ++c)
               for (int j = 0; j < nks; ++j)
-                tc_mma_bf16(acc, umma_desc_noswz(a_tap + 2 * j * a_chunk, a_chunk, 128),
-                            umma_desc_noswz(b_at + 2 * j * b_chunk, b_chunk, 128), idesc,
-                            (cb | r | c | j) != 0 ? 1u : 0u);
-            }
-          tc_commit(&empty[s]);
-          if (cb + 1 == ncb) tc_commit(&tfull[a]);
+                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(r * wp + c + j * a_ks16),
+                                  bd + static_cast<uint64_t>((r * ka + c) * b_tap16 + j * b_ks16),
+                                  idesc, (cb | r | c | j) != 0 ? 1u : 0u);
         }
+        tc_commit_elect(&empty[s]);
+        if (cb + 1 == ncb) tc_commit_elect(&tfull[a]);
         __syncwarp();
       }
     }
@@ -176,7 +211,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
       const bool ok = p_row < rt * wp && ow < p.wo && oh < p.ho;
       const size_t m = (static_cast<size_t>(img) * p.ho + oh) * p.wo + ow;
       const size_t rowoff = m * d.cout;
-      mbar_wait(&tfull[a], static_cast<uint32_t>(i / nacc) & 1);
+      HL_WAIT(w_wait, &tfull[a], static_cast<uint32_t>(i / nacc) & 1);
       tc_fence_after();
       for (int c = 0; c < nch; ++c) {
         float v[32];
@@ -186,7 +221,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[a]);
         }
-        if (!ok) continue;
+        if (!ok || (p.dbg & 1)) continue;
         uint4 rv[4];
         if (p.res) {
 #pragma unroll
@@ -253,6 +288,10 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
       }
     }
   }
+#undef HL_WAIT
+  if (prof && lane == 0 && (warp == 0 || warp == HL_MMA_WARP || warp == 1))
+    printf("[conv_tc prof] tiles=%d nk=%d warp=%d total=%lld wait=%lld wait2=%lld\n", tiles, ncb,
+           warp, clock64() - t_begin, w_wait, w_wait2);
   tc_fence_before();
   __syncthreads();
   if (warp == HL_MMA_WARP) {
@@ -373,6 +412,11 @@ cudaError_t init_conv_halo() {
 // cout_max); the active subnet's extents and A map come from its OpDesc.
 cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps,
                              cudaStream_t s) {
+  static const int dbg = [] {
+    const char* e = getenv("SSN_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  p.dbg = dbg;
   p.hb_rows = halo_b_rows(p.cout_max);
   p.hb_chunks = halo_b_chunks(p.cin_max);
   p.h_stages = halo_stages(p.w_, p.k_max, p.cin_max, p.cout_max);

@@ -122,7 +122,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
   const int tiles = mt * nt;
   if (static_cast<int>(blockIdx.x) >= tiles) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp index through shfl: the compiler then knows it is warp-uniform, so
+  // role branches stay uniform and MMA/TMA operands live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
 
   const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
   const int cblocks = (d.cin + TC_BK - 1) / TC_BK;
@@ -305,7 +308,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int nv = colok ? min(8, d.cout - col) : 0;
       const bool vec = EPI != 2 || (nv == 8 && (d.cout & 7) == 0);
       float v[32];
-      tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+      if (prof) {
+        const long long t0 = clock64();
+        tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+        w_wait2 += clock64() - t0;
+      } else {
+        tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+      }
       float4* srow = reinterpret_cast<float4*>(stg + lane * TC_STG_LD);
 #pragma unroll
       for (int q = 0; q < 8; ++q)
@@ -380,9 +389,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ============================================================ MMA issuer
-    const bool leader = elect_one();
+    // Converged warp, elected lane issues (tc_mma_bf16_elect); descriptors
+    // are a base plus 16-byte-unit offsets (SW128: K step = +32 B).
     const uint32_t idesc = umma_idesc_bf16(bn);
-    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    const uint64_t a_base = umma_desc_sw128(smem_u32(sA));
+    const uint64_t b_base = umma_desc_sw128(smem_u32(sB));
     int g = 0, i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int a = i % NACC;
@@ -408,23 +419,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         tc_fence_after();
         const int nsub = min(KPS, nk - kb);
-        if (leader) {
 #pragma unroll
-          for (int j = 0; j < KPS; ++j) {
-            if (j < nsub) {
-              const uint64_t ad = umma_desc_sw128(a0 + (s * KPS + j) * C::A_BYTES);
-              const uint64_t bd = umma_desc_sw128(b0 + (s * KPS + j) * C::B_BYTES);
+        for (int j = 0; j < KPS; ++j) {
+          if (j < nsub) {
+            const uint64_t ad = a_base + static_cast<uint64_t>(((s * KPS + j) * C::A_BYTES) >> 4);
+            const uint64_t bd = b_base + static_cast<uint64_t>(((s * KPS + j) * C::B_BYTES) >> 4);
 #pragma unroll
-              for (int kk = 0; kk < TC_BK / 16; ++kk)
-                if (!(p.dbg & 2))
-                  tc_mma_bf16(acc, ad + static_cast<uint64_t>(kk * 2),
-                              bd + static_cast<uint64_t>(kk * 2), idesc,
-                              ((kb + j) | kk) != 0 ? 1u : 0u);
-            }
+            for (int kk = 0; kk < TC_BK / 16; ++kk)
+              if (!(p.dbg & 2))
+                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(kk * 2),
+                                  bd + static_cast<uint64_t>(kk * 2), idesc,
+                                  ((kb + j) | kk) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
-          if (kb + KPS >= nk) tc_commit(&tfull[a]);
         }
+        tc_commit_elect(&empty[s]);
+        if (kb + KPS >= nk) tc_commit_elect(&tfull[a]);
         __syncwarp();
       }
     }

@@ -23,6 +23,11 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (64, 28, 28, 176, 176, 176, 176, 3, 1, 0),
     (1, 7, 7, 64, 64, 64, 64, 1, 1, 0),
     (8, 14, 14, 64, 64, 64, 64, 1, 1, 0),
+    (64, 56, 56, 56, 88, 56, 88, 3, 1, 0),
+    (1, 14, 14, 16, 16, 16, 16, 3, 1, 0),
+    (1, 56, 56, 88, 88, 88, 88, 3, 1, 0),
+    (64, 56, 56, 88, 88, 256, 256, 1, 1, 0),   # case3 without the residual
+    (64, 56, 56, 256, 256, 256, 256, 1, 1, 0), # wide in, wide out
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
