@@ -268,96 +268,183 @@ __global__ void conv_f32_kernel(ConvParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// bf16 depthwise k x k conv (OFA elastic kernel: centre crop of k_max) fused
-// with SubnetNorm + activation.  Weights tap-major [k_max*k_max][c_max] so a
-// thread's 8 channels of one tap are one 16-byte load.  Each thread computes
-// DW_Q horizontally adjacent outputs of one 8-channel group: per kernel row
-// it loads the (DW_Q-1)*stride + k input pixels and k weights ONCE and reuses
-// them from registers (k=7: 17 loads per row instead of 98 per 4 outputs).
-// Consecutive threads walk channel groups of one pixel quad (coalesced NHWC).
+// bf16 depthwise k x k conv (OFA elastic kernel: centre crop of k_max = 7)
+// fused with SubnetNorm + activation; weights tap-major [k_max^2][c_max].
+//
+// Shared-memory tiled: a CTA owns an 8 x 8 output tile of 32 channels.  It
+// stages the input halo tile ((8-1)*S + k)^2 pixels x 64 B once with
+// coalesced 16-byte loads (zero fill at the image border / channel tail) and
+// the k x k x 32 weights, then each thread computes 4 adjacent outputs of 2
+// channels with packed fp32x2 FMAs (FFMA2) from shared memory.  Every input
+// byte leaves HBM once (halo re-reads hit L2: neighbouring tiles of a channel
+// chunk are adjacent in the launch order).  The previous per-thread register
+// scheme re-loaded each input element ~17x through L1 and ran at ~0.1 of the
+// HBM roofline on OFA-MBv3.
+// Bank layout: the two half-warps read rows S apart; the padded row stride
+// (== 64 mod 128 bytes per S rows) puts them in disjoint banks.
 
-constexpr int DW_Q = 4;  // adjacent outputs per thread
-constexpr int DW_C = 4;  // channels per thread (8-byte vectors keep registers low)
+constexpr int DWT_CC = 32;  // channels per CTA
 
-__device__ __forceinline__ void bf16x4_to_f32(const uint2& u, float* f) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-  const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+// Tile geometry per stride: TH x TW outputs, QW adjacent outputs per thread,
+// 16 channel pairs x (TH * TW / QW) threads = 256.
+template <int S>
+struct DwTile {
+  static constexpr int TH = S == 1 ? 16 : 8;
+  static constexpr int TW = 8;
+  static constexpr int QW = S == 1 ? 8 : 4;
+  static constexpr int IH = (TH - 1) * S + 7;  // staged rows/cols for k_max 7
+  static constexpr int IW = (TW - 1) * S + 7;
+  static constexpr int PIX = DWT_CC * 4;       // fp32 pixel: 128 B
+  static constexpr int IN_BYTES = IH * IW * PIX;
+  static constexpr int W_BYTES = 49 * PIX;
+  static constexpr int SMEM = IN_BYTES + W_BYTES;
+  static_assert(16 * TH * (TW / QW) == 256, "256 threads per tile");
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long o;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(o)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&o);
 }
 
-template <int STRIDE>
+template <int S, int K>
+__device__ __forceinline__ void dw_tile_compute(const uint8_t* tile, const uint8_t* wts, int cp,
+                                                int orow, int ocol0,
+                                                float2 (&acc)[DwTile<S>::QW]) {
+  using T = DwTile<S>;
+  constexpr int SEG = (T::QW - 1) * S + K;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const uint8_t* row = tile + ((orow * S + r) * T::IW + ocol0 * S) * T::PIX + cp * 8;
+    float2 in[SEG];
+#pragma unroll
+    for (int t = 0; t < SEG; ++t) in[t] = *reinterpret_cast<const float2*>(row + t * T::PIX);
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const float2 w = *reinterpret_cast<const float2*>(wts + (r * K + s) * T::PIX + cp * 8);
+#pragma unroll
+      for (int q = 0; q < T::QW; ++q) acc[q] = ffma2(in[q * S + s], w, acc[q]);
+    }
+  }
+}
+
+__device__ __forceinline__ void st_f32x8(uint8_t* dst, const uint4& v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+  const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+  const float2 c = __bfloat1622float2(h[2]), e = __bfloat1622float2(h[3]);
+  reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, e.x, e.y);
+}
+
+template <int S>
 __global__ void __launch_bounds__(256) dw_bf16_kernel(ConvParams p) {
-  constexpr int DW_SEG = (DW_Q - 1) * STRIDE + 7;  // input pixels per row for k_max = 7
+  using T = DwTile<S>;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  uint8_t* tile = dsm;                 // [IH][IW][32] fp32
+  uint8_t* wts = dsm + T::IN_BYTES;    // [k*k][32] fp32
   const OpDims d = load_desc(p.row, p.fixed, p.op);
-  const int C = d.cout, G = C / DW_C;
+  const int C = d.cout;
   const int k = d.k, pad = d.pad, off = (p.k_max - k) / 2;
+  const int tw_n = (p.wo + T::TW - 1) / T::TW, th_n = (p.ho + T::TH - 1) / T::TH;
+  const int chunks = (p.cout_max + DWT_CC - 1) / DWT_CC;
+  // launch order (img, chunk, th, tw): spatial neighbours of one channel chunk
+  // run together, so halo re-reads are L2 hits
+  long b = blockIdx.x;
+  const int tw = static_cast<int>(b % tw_n);
+  b /= tw_n;
+  const int th = static_cast<int>(b % th_n);
+  b /= th_n;
+  const int cb = static_cast<int>(b % chunks);
+  const int img = static_cast<int>(b / chunks);
+  const int c0 = cb * DWT_CC;
+  if (c0 >= C) return;  // WeightSlice: chunks past the active width
+  const int oh0 = th * T::TH, ow0 = tw * T::TW;
+  const int ih0 = oh0 * S - pad, iw0 = ow0 * S - pad;
+  const int ih_a = (T::TH - 1) * S + k, iw_a = (T::TW - 1) * S + k;  // staged extent, active k
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
   const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w);
-  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y);
-  const int wq = (p.wo + DW_Q - 1) / DW_Q;
-  const long total = static_cast<long>(p.n) * p.ho * wq * G;
-  const int nseg = (DW_Q - 1) * STRIDE + k;
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % G);
-    long rest = i / G;
-    const int qx = static_cast<int>(rest % wq);
-    rest /= wq;
-    const int oh = static_cast<int>(rest % p.ho);
-    const int img = static_cast<int>(rest / p.ho);
-    const int ow0 = qx * DW_Q;
-    const int iw0 = ow0 * STRIDE - pad;
-    float acc[DW_Q][DW_C];
+  const int tid = threadIdx.x;
+
+  // stage the input halo tile, converted to fp32 once.  Thread -> (16-byte
+  // quarter q of a pixel's 32 channels, column, row-in-block); all of its
+  // loads are issued before any conversion (memory-level parallelism), no
+  // integer division, and the two 16-byte halves of each fp32 quarter are
+  // written in pixel-parity order so a warp's stores hit all 8 bank groups.
+  {
+    constexpr int CP = S == 1 ? 16 : 32;  // columns per row block (>= IW)
+    constexpr int RP = 64 / CP;           // rows per block
+    constexpr int IT = (T::IH + RP - 1) / RP;
+    const int q = tid & 3, pl = tid >> 2;
+    const int col = pl & (CP - 1), rsub = pl / CP;
+    const int iw = iw0 + col;
+    const bool colok = col < iw_a && iw >= 0 && iw < p.w_ && c0 + q * 8 < C;
+    const __nv_bfloat16* xs = x + (static_cast<long>(img) * p.h * p.w_ + iw) * C + c0 + q * 8;
+    uint4 v[IT];
 #pragma unroll
-    for (int q = 0; q < DW_Q; ++q)
+    for (int it = 0; it < IT; ++it) {
+      const int r = it * RP + rsub;
+      const int ih = ih0 + r;
+      v[it] = make_uint4(0, 0, 0, 0);
+      if (colok && r < ih_a && ih >= 0 && ih < p.h)
+        v[it] = __ldg(reinterpret_cast<const uint4*>(xs + static_cast<long>(ih) * p.w_ * C));
+    }
+    const int h0 = (col & 1) * 16, h1 = 16 - h0;
 #pragma unroll
-      for (int c = 0; c < DW_C; ++c) acc[q][c] = 0.f;
-    for (int r = 0; r < k; ++r) {
-      const int ih = oh * STRIDE - pad + r;
-      if (ih < 0 || ih >= p.h) continue;
-      const __nv_bfloat16* xrow = x + (static_cast<long>(img * p.h + ih) * p.w_) * C + g * DW_C;
-      float seg[DW_SEG][DW_C];
-#pragma unroll
-      for (int t = 0; t < DW_SEG; ++t) {
-        const int iw = iw0 + t;
-        if (t < nseg && iw >= 0 && iw < p.w_) {
-          bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(xrow + static_cast<long>(iw) * C)), seg[t]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < DW_C; ++c) seg[t][c] = 0.f;
-        }
-      }
-      const __nv_bfloat16* wrow =
-          w + static_cast<long>((r + off) * p.k_max + off) * p.cout_max + g * DW_C;
-#pragma unroll
-      for (int s = 0; s < 7; ++s) {
-        if (s >= k) break;
-        float wv[DW_C];
-        bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(wrow + static_cast<long>(s) * p.cout_max)), wv);
-#pragma unroll
-        for (int q = 0; q < DW_Q; ++q)
-#pragma unroll
-          for (int c = 0; c < DW_C; ++c) acc[q][c] += seg[q * STRIDE + s][c] * wv[c];
+    for (int it = 0; it < IT; ++it) {
+      const int r = it * RP + rsub;
+      if (r < ih_a && col < iw_a) {
+        uint8_t* dst = tile + (r * T::IW + col) * T::PIX + q * 32;
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[it]);
+        const float2 a = __bfloat1622float2(hv[0]), bq = __bfloat1622float2(hv[1]);
+        const float2 c = __bfloat1622float2(hv[2]), e = __bfloat1622float2(hv[3]);
+        const float4 lo = make_float4(a.x, a.y, bq.x, bq.y), hi = make_float4(c.x, c.y, e.x, e.y);
+        *reinterpret_cast<float4*>(dst + h0) = h0 ? hi : lo;
+        *reinterpret_cast<float4*>(dst + h1) = h0 ? lo : hi;
       }
     }
-    float sc[DW_C], sh[DW_C];
+  }
+  for (int idx = tid; idx < k * k * 4; idx += 256) {
+    const int q = idx & 3, tap = idx >> 2;
+    const int r = tap / k, s = tap - r * k;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c0 + q * 8 < C)
+      v = __ldg(reinterpret_cast<const uint4*>(w + static_cast<long>((r + off) * p.k_max + s + off) *
+                                                       p.cout_max + c0 + q * 8));
+    st_f32x8(wts + tap * T::PIX + q * 32, v);
+  }
+  __syncthreads();
+
+  const int cp = tid & 15;  // channel pair
+  const int pg = tid >> 4;
+  const int orow = S == 1 ? pg : (pg & 7);
+  const int ocol0 = S == 1 ? 0 : (pg >> 3) * T::QW;
+  float2 acc[T::QW];
 #pragma unroll
-    for (int c = 0; c < DW_C; ++c) {
-      sc[c] = d.scale ? d.scale[g * DW_C + c] : 1.f;
-      sh[c] = d.shift ? d.shift[g * DW_C + c] : 0.f;
-    }
+  for (int q = 0; q < T::QW; ++q) acc[q] = make_float2(0.f, 0.f);
+  if (k == 3)
+    dw_tile_compute<S, 3>(tile, wts, cp, orow, ocol0, acc);
+  else if (k == 5)
+    dw_tile_compute<S, 5>(tile, wts, cp, orow, ocol0, acc);
+  else
+    dw_tile_compute<S, 7>(tile, wts, cp, orow, ocol0, acc);
+
+  const int c = c0 + 2 * cp;
+  const int oh = oh0 + orow;
+  if (c >= C || oh >= p.ho) return;
+  const float2 sc = d.scale ? make_float2(d.scale[c], d.scale[c + 1]) : make_float2(1.f, 1.f);
+  const float2 sh = d.shift ? make_float2(d.shift[c], d.shift[c + 1]) : make_float2(0.f, 0.f);
+  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y) + (static_cast<long>(img * p.ho + oh) * p.wo) * C + c;
 #pragma unroll
-    for (int q = 0; q < DW_Q; ++q) {
-      const int ow = ow0 + q;
-      if (ow >= p.wo) break;
-      float o[DW_C];
-#pragma unroll
-      for (int c = 0; c < DW_C; ++c) o[c] = act_apply(acc[q][c] * sc[c] + sh[c], p.act);
-      uint2 pk;
-      pk.x = pack_bf16x2(o[0], o[1]);
-      pk.y = pack_bf16x2(o[2], o[3]);
-      *reinterpret_cast<uint2*>(y + (static_cast<long>(img * p.ho + oh) * p.wo + ow) * C + g * DW_C) = pk;
-    }
+  for (int q = 0; q < T::QW; ++q) {
+    const int ow = ow0 + ocol0 + q;
+    if (ow >= p.wo) break;
+    const float2 v = ffma2(acc[q], sc, sh);
+    *reinterpret_cast<uint32_t*>(y + static_cast<long>(ow) * C) =
+        pack_bf16x2(act_apply(v.x, p.act), act_apply(v.y, p.act));
   }
 }
 
@@ -517,13 +604,21 @@ cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
-  const long work = static_cast<long>(p.n) * p.ho * ((p.wo + DW_Q - 1) / DW_Q) * (p.cout_max / DW_C);
-  if (p.stride == 2)
-    dw_bf16_kernel<2><<<grid_for(work, 256), 256, 0, s>>>(p);
-  else
-    dw_bf16_kernel<1><<<grid_for(work, 256), 256, 0, s>>>(p);
+template <int S>
+static cudaError_t launch_dw_tiles(const ConvParams& p, cudaStream_t s) {
+  using T = DwTile<S>;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      dw_bf16_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+  if (attr != cudaSuccess) return attr;
+  const long tiles = static_cast<long>(p.n) * ((p.ho + T::TH - 1) / T::TH) *
+                     ((p.wo + T::TW - 1) / T::TW) * ((p.cout_max + DWT_CC - 1) / DWT_CC);
+  dw_bf16_kernel<S><<<static_cast<unsigned>(tiles), 256, T::SMEM, s>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
+  if (p.k_max > 7 || (p.stride != 1 && p.stride != 2)) return cudaErrorInvalidValue;
+  return p.stride == 2 ? launch_dw_tiles<2>(p, s) : launch_dw_tiles<1>(p, s);
 }
 
 cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
