@@ -278,6 +278,7 @@ def run_ours(args, rank, world, local_rank):
     act = measure_actuation(eng, torch, stream, xs[0], B)
 
     roof = live_roofline(eng, desc, cfgs, B, peaks, ssn)
+    families = None if args.no_families else family_rows(ssn, peaks, local_rank)
     cpu = None
     if world == 1 and not args.no_cpu:
         n, el, cores = cpu_sample(args.image, 1, min_seconds=args.cpu_seconds, max_rounds=8)
@@ -300,6 +301,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline_detail": roof,
         "actuation_us": act,
         "per_subnet": per_subnet,
+        "families": families,
         "cpu_baseline": cpu,
         "engine": {k: v for k, v in eng.stats().items()
                    if k in ("weight_bytes", "norm_table_bytes", "arena_bytes", "graphs_built")},
@@ -339,12 +341,45 @@ def measure_actuation(eng, torch, stream, x, B):
             "switch_overhead_us": switched - steady}
 
 
+def family_rows(ssn, peaks, device):
+    """BASELINE.json configs 3 and 5 on the same engine API (untimed region):
+    OFA-MobileNetV3-w1.2 at bs256 (224^2 uint8 images) and the width/depth-
+    sliced BERT-base encoder at bs64 x seq128, min/mid/max subnets.  Latency is
+    a CUDA-graph replay (ssn_profile_latency); roofline_frac = sum over ops of
+    max(flops / tensor peak, bytes / HBM peak) / measured latency."""
+    out = {}
+    specs = ((ssn.FAMILY_OFA_MBV3, "ofa_mbv3_w1.2", 256, 224, 1000, "images/s"),
+             (ssn.FAMILY_BERT, "bert_base_seq128", 64, 128, 2, "sequences/s"))
+    for fam, name, B, size, ncls, unit in specs:
+        desc = ssn.make_desc(fam, ssn.DTYPE_BF16, image_size=size, num_classes=ncls, max_batch=B,
+                             seed=0, input_format=ssn.INPUT_U8_NHWC)
+        eng = ssn.Engine(desc, device=device)
+        names = ("min", "mid", "max")
+        cfgs = [ssn.supernets.preset(fam, n) for n in names]
+        for i, c in enumerate(cfgs):
+            eng.register_subnet(i, c)
+        eng.prepare([B])
+        row = {"batch": B, "unit": unit}
+        for i, n in enumerate(names):
+            us = eng.profile_latency(i, B, iters=10)
+            cost = ssn.plan_cost(desc, cfgs[i])
+            roof = sum(max(p["flops"] * B / (peaks["tc_sust"] * 1e12),
+                           (p["bytes"] * B + p["weight_bytes"]) / (peaks["hbm"] * 1e9))
+                       for p in cost["per_op"] if p is not None)
+            row[n] = {"us": round(us, 1), "value": round(B / (us * 1e-6), 1),
+                      "roofline_frac": round(roof / (us * 1e-6), 4)}
+        eng.close()
+        out[name] = row
+    return out
+
+
 def live_roofline(eng, desc, cfgs, B, peaks, ssn):
     """Per-op CUDA-event times of each sweep subnet at batch B; the dominant
     kernel family is the tcgen05 WeightSlice conv (OP_CONV / OP_LINEAR)."""
     tot_f = tot_t = tot_b = 0.0
     roof_t = meas_t = 0.0
     conv_t = all_t = 0.0
+    n_conv = 0
     largest = None
     for sid, cfg in enumerate(cfgs):
         cost = ssn.plan_cost(desc, cfg)
@@ -360,6 +395,7 @@ def live_roofline(eng, desc, cfgs, B, peaks, ssn):
             roof_t += max(f / (peaks["tc_sust"] * 1e12), byts / (peaks["hbm"] * 1e9))
             meas_t += t
             if r["kind"] in (1, 5):
+                n_conv += 1
                 conv_t += t
                 tot_f += f
                 tot_b += byts
@@ -369,8 +405,14 @@ def live_roofline(eng, desc, cfgs, B, peaks, ssn):
                     largest["f"] += f
                     largest["t"] += t
     achieved = tot_f / tot_t / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):  # ncu DRAM bytes per conv_tc launch, same sweep (committed capture)
+        with open(tfile) as f:
+            traffic = json.load(f).get("conv_tc", {}).get("dram_bytes_per_launch")
     head = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["tc_sust"],
-            "unit": "TFLOP/s", "frac": round(achieved / peaks["tc_sust"], 4), "traffic": None,
+            "unit": "TFLOP/s", "frac": round(achieved / peaks["tc_sust"], 4), "traffic": traffic,
+            "algorithmic_bytes_per_launch": round(tot_b / max(n_conv, 1)),
             "kernel": "conv_tc_kernel (tcgen05 WeightSlice implicit GEMM), all launches of the "
                       f"{{{','.join(SUBNETS)}}} sweep at bs{B}",
             "peak_source": f"{peaks['src']} bf16_tflops_sustained"}
@@ -396,6 +438,8 @@ def main():
     ap.add_argument("--image", type=int, default=224)
     ap.add_argument("--sweep", action="store_true", help="also profile bs 1/8/64/256")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-families", action="store_true",
+                    help="skip the OFA-MBv3 / BERT rows (configs 3 and 5)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

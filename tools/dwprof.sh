@@ -1,4 +1,4 @@
-timeout 400 python -m pytest tests -m gpu -q -x -k "mbv3" 2>&1 | tail -1
-python tools/profile_family.py --family mbv3 --batches 256 --iters 20 2>&1 | tail -3
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active,launch__grid_size --clock-control none -k regex:dw_bf16 --csv --log-file gpurun_out/dw_metrics.csv python tools/prof_forward.py --family mbv3 --batch 256 --steps 1 --warmup 0 --subnets max > /dev/null 2>&1
+
+
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active,launch__grid_size --clock-control none -k regex:dw --csv --log-file gpurun_out/dw_metrics.csv python tools/prof_forward.py --family mbv3 --batch 256 --steps 1 --warmup 0 --subnets max > /dev/null 2>&1
 python tools/dw_table.py gpurun_out/dw_metrics.csv
