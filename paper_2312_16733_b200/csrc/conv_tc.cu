@@ -50,16 +50,24 @@ constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 320
 constexpr int TC_STG_LD = 36;  // padded fp32 row of the 32x32 epilogue transpose tile
 constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
 
-template <int BN_MAX, int STAGES, int KPS>
+// Resident-B mode (RESB): when the whole active weight slice is ONE N tile
+// of <= TC_RB_BYTES (narrow 1x1 convs: 88->256, 256->88, 64->256 ...), it is
+// loaded into shared memory once per CTA and only A streams through the
+// ring.  Re-streaming B per tile was ~40% of such a layer's time
+// (SSN_TC_DEBUG=8 isolation) because every tile re-read the same weights.
+constexpr int TC_RB_BYTES = 96 * 1024;
+
+template <int BN_MAX, int STAGES, int KPS, int RESB = 0>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN_MAX * TC_BK * 2;
-  static constexpr int STAGE_BYTES = KPS * (A_BYTES + B_BYTES);
+  static constexpr int RB_BLOCKS = RESB ? TC_RB_BYTES / B_BYTES : 0;
+  static constexpr int STAGE_BYTES = KPS * (A_BYTES + (RESB ? 0 : B_BYTES));
   // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
   // (max 4), so the MMA can run several tiles ahead of the epilogue.
   static constexpr int NACC = 512 / BN_MAX > 4 ? 4 : 512 / BN_MAX;
-  static constexpr int SMEM =
-      1024 + STAGES * STAGE_BYTES + TC_STG_BYTES + (2 * STAGES + 2 * NACC) * 8 + 16;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + (RESB ? TC_RB_BYTES : 0) +
+                              TC_STG_BYTES + (2 * STAGES + 2 * NACC + 1) * 8 + 16;
   static_assert(SMEM <= 232448, "operand ring exceeds 227 KB of shared memory");
 };
 
@@ -97,23 +105,25 @@ struct EpiIn {
 // ragged output slice (cout % 8 != 0; BERT head).  One instance per epilogue
 // keeps each compact: an inlined erff/tanhf + scalar tail tripled the SASS of
 // the ReLU kernel and halved its throughput through I-cache misses.
-template <int BN_MAX, int STAGES, int KPS, int EPI>
+template <int BN_MAX, int STAGES, int KPS, int EPI, int RESB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
-  using C = TcCfg<BN_MAX, STAGES, KPS>;
+  using C = TcCfg<BN_MAX, STAGES, KPS, RESB>;
   constexpr int NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned for SW128; offset arithmetic on smem_raw keeps the shared
   // address space visible to the compiler
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                 // [STAGES][KPS] A boxes
-  uint8_t* sB = smem + STAGES * KPS * C::A_BYTES;     // [STAGES][KPS] B boxes
-  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES + TC_STG_BYTES);
+  uint8_t* sB = smem + STAGES * KPS * C::A_BYTES;     // [STAGES][KPS] B boxes | RESB: [nk] blocks
+  uint8_t* epi_base = smem + STAGES * C::STAGE_BYTES + (RESB ? TC_RB_BYTES : 0);
+  float* epi_stage = reinterpret_cast<float*>(epi_base);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_base + TC_STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [NACC]
   uint64_t* tempty = tfull + NACC;   // [NACC]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
+  uint64_t* bfull = tempty + NACC;  // RESB: the resident weight slice landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
@@ -140,6 +150,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], TC_EPI_WARPS / 2);  // the 4 warps of the owning group
     }
+    mbar_init(bfull, 1);
     fence_mbar_init();
     tma_prefetch(&wmap);
     tma_prefetch(&dp->amap);
@@ -159,7 +170,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool leader = elect_one();
     const CUtensorMap* amap = &dp->amap;
     const int hwo = p.ho * p.wo;
-    const uint32_t kb_bytes = static_cast<uint32_t>(C::A_BYTES + bn * TC_BK * 2);
+    const uint32_t kb_bytes = static_cast<uint32_t>(C::A_BYTES + (RESB ? 0 : bn * TC_BK * 2));
+    if (RESB && leader) {
+      // the whole (single-N-tile) weight slice, once per CTA: block kb = (tap, channel block)
+      if (p.dbg & 8) {
+        mbar_arrive(bfull);
+      } else {
+        mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nk * bn * TC_BK * 2));
+        int tr = 0, ts = 0, cb = 0;
+        for (int kb = 0; kb < nk; ++kb) {
+          tma_load_3d(sB + kb * C::B_BYTES, &wmap, bfull, cb * TC_BK,
+                      (tr + koff) * p.k_max + (ts + koff), 0);
+          if (++cb == cblocks) {
+            cb = 0;
+            if (++ts == ka) {
+              ts = 0;
+              ++tr;
+            }
+          }
+        }
+      }
+    }
     int g = 0;  // stage counter (ring position)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int m0 = (t / nt) * TC_BM;
@@ -183,7 +214,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int nsub = min(KPS, nk - kb);
         if (leader) {
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES);
-          const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
+          const uint32_t b_tx = ((p.dbg & 8) || RESB) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
           const uint32_t tx = (p.dbg & 12) ? nsub * (a_tx + b_tx) : nsub * kb_bytes;
           if (tx) mbar_arrive_expect_tx(&full[s], tx);
           else mbar_arrive(&full[s]);
@@ -195,7 +226,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (!(p.dbg & 4))
                 tma_im2col_4d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0,
                               img, static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
-              if (!(p.dbg & 8))
+              if (!RESB && !(p.dbg & 8))
                 tma_load_3d(sB + (s * KPS + j) * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
                             (tr + koff) * p.k_max + (ts + koff), n0);
             }
@@ -394,6 +425,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t idesc = umma_idesc_bf16(bn);
     const uint64_t a_base = umma_desc_sw128(smem_u32(sA));
     const uint64_t b_base = umma_desc_sw128(smem_u32(sB));
+    if (RESB) {
+      mbar_wait(bfull, 0);
+      tc_fence_after();
+    }
     int g = 0, i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int a = i % NACC;
@@ -423,7 +458,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < KPS; ++j) {
           if (j < nsub) {
             const uint64_t ad = a_base + static_cast<uint64_t>(((s * KPS + j) * C::A_BYTES) >> 4);
-            const uint64_t bd = b_base + static_cast<uint64_t>(((s * KPS + j) * C::B_BYTES) >> 4);
+            const uint64_t bd =
+                b_base + static_cast<uint64_t>(((RESB ? kb + j : s * KPS + j) * C::B_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 16; ++kk)
               if (!(p.dbg & 2))
@@ -544,18 +580,20 @@ int choose_bn(int cout_max, long M) {
 }
 
 // Instances (BN_MAX, STAGES, K blocks per stage): the operand ring plus the
-// 36 KB epilogue staging fill the 227 KB of shared memory.
-#define SSN_TC_INSTANCES(X) X(64, 7, 1) X(128, 5, 1) X(256, 3, 1)
+// 36 KB epilogue staging fill the 227 KB of shared memory; resident-B
+// instances trade ring stages for the 96 KB weight block.
+#define SSN_TC_INSTANCES(X) X(64, 7, 1, 0) X(128, 5, 1, 0) X(256, 3, 1, 0) \
+  X(64, 5, 1, 1) X(128, 5, 1, 1) X(256, 5, 1, 1)
 
 cudaError_t init_conv_tc() {
-#define SSN_TC_ATTR(BN, ST, KPS)                                                          \
+#define SSN_TC_ATTR(BN, ST, KPS, RB)                                                      \
   {                                                                                       \
-    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, KPS, 0>,            \
-                                               conv_tc_kernel<BN, ST, KPS, 1>,            \
-                                               conv_tc_kernel<BN, ST, KPS, 2>};           \
+    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, KPS, 0, RB>,        \
+                                               conv_tc_kernel<BN, ST, KPS, 1, RB>,        \
+                                               conv_tc_kernel<BN, ST, KPS, 2, RB>};       \
     for (auto fn : fns) {                                                                 \
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           TcCfg<BN, ST, KPS>::SMEM);                     \
+                                           TcCfg<BN, ST, KPS, RB>::SMEM);                 \
       if (e != cudaSuccess) return e;                                                     \
     }                                                                                     \
   }
@@ -564,17 +602,17 @@ cudaError_t init_conv_tc() {
   return cudaSuccess;
 }
 
-template <int BN_MAX, int STAGES, int KPS>
+template <int BN_MAX, int STAGES, int KPS, int RESB>
 static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
-  using C = TcCfg<BN_MAX, STAGES, KPS>;
+  using C = TcCfg<BN_MAX, STAGES, KPS, RESB>;
   const long tiles = static_cast<long>((p.M + TC_BM - 1) / TC_BM) * ((p.cout_max + p.bn - 1) / p.bn);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   if (p.act > 2 || (p.cout_max & 7) != 0 || p.ragged)
-    conv_tc_kernel<BN_MAX, STAGES, KPS, 2><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    conv_tc_kernel<BN_MAX, STAGES, KPS, 2, RESB><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   else if (p.act == 2)
-    conv_tc_kernel<BN_MAX, STAGES, KPS, 1><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    conv_tc_kernel<BN_MAX, STAGES, KPS, 1, RESB><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   else
-    conv_tc_kernel<BN_MAX, STAGES, KPS, 0><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    conv_tc_kernel<BN_MAX, STAGES, KPS, 0, RESB><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
   return cudaGetLastError();
 }
 
@@ -585,9 +623,14 @@ cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cuda
   }();
   ConvParams p = p_in;
   p.dbg = dbg;
-  if (p.bn <= 64) return launch_impl<64, 7, 1>(p, wmap, s);
-  if (p.bn <= 128) return launch_impl<128, 5, 1>(p, wmap, s);
-  return launch_impl<256, 3, 1>(p, wmap, s);
+  // Resident B: the max-shape slice is one N tile (so is every subnet's) and
+  // all its K blocks fit TC_RB_BYTES.
+  const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
+  const bool resb = !(p.dbg & 512) && p.cout_max <= p.bn && nk_max * p.bn * TC_BK * 2 <= TC_RB_BYTES;
+  if (p.bn <= 64) return resb ? launch_impl<64, 5, 1, 1>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
+  if (p.bn <= 128)
+    return resb ? launch_impl<128, 5, 1, 1>(p, wmap, s) : launch_impl<128, 5, 1, 0>(p, wmap, s);
+  return resb ? launch_impl<256, 5, 1, 1>(p, wmap, s) : launch_impl<256, 3, 1, 0>(p, wmap, s);
 }
 
 }  // namespace ssn
