@@ -277,6 +277,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // EPI 0/1: SubnetNorm rows and biases are 16-byte aligned (engine
       // tables; the operator API routes unaligned vectors to EPI 2)
       const bool v4 = EPI != 2 || (sc_vec && nv == 8);
+      if (p.dbg & 4096) {  // profiling: constant SubnetNorm row
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          in.sc[q] = 1.f;
+          in.sh[q] = 0.f;
+        }
+      } else {
       if (d.scale && v4) {
         const float4 s0 = __ldg(reinterpret_cast<const float4*>(d.scale + col));
         const float4 s1 = __ldg(reinterpret_cast<const float4*>(d.scale + col + 4));
@@ -297,7 +304,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int q = 0; q < 8; ++q)
           in.sh[q] = d.shift ? __ldg(d.shift + (EPI == 2 ? min(col + q, d.cout - 1) : col + q)) : 0.f;
       }
-      if (p.res) {
+      }
+      if (p.res && !(p.dbg & 2048)) {
 #pragma unroll
         for (int r4 = 0; r4 < 4; ++r4) {
           const int m = m0 + rsub + 8 * r4;
@@ -308,6 +316,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     };
+    // epilogue flags hoisted out of the chunk loop (uniform registers)
+    const bool has_res = p.res != nullptr;
+    const bool res_post = p.res_post != 0;
+    const int act = p.act;
+    const bool out_f32 = p.out_f32 != 0;
     int i = group;  // local tile ordinal
     int t = blockIdx.x + i * static_cast<int>(gridDim.x);
     int c = 0;
@@ -356,62 +369,88 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
       }
+      const long long tsec = prof ? clock64() : 0;
       if (colok && !(p.dbg & 1)) {
+        // All four rows' staging reads first, then straight-line math, then
+        // the predicated stores: one dependency chain per chunk instead of
+        // four (the per-row `continue` + uniform-flag branches serialised
+        // LDS -> FFMA -> STG and left the epilogue latency-bound).
+        float o[4][8];
 #pragma unroll
         for (int r4 = 0; r4 < 4; ++r4) {
-          const int rr = rsub + 8 * r4;
-          const int m = m0 + rr;
-          if (m >= p.M) continue;
-          const float4* sp = reinterpret_cast<const float4*>(stg + rr * TC_STG_LD + seg * 8);
+          const float4* sp = reinterpret_cast<const float4*>(stg + (rsub + 8 * r4) * TC_STG_LD + seg * 8);
           const float4 lo = sp[0], hi = sp[1];
-          float o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+          o[r4][0] = lo.x; o[r4][1] = lo.y; o[r4][2] = lo.z; o[r4][3] = lo.w;
+          o[r4][4] = hi.x; o[r4][5] = hi.y; o[r4][6] = hi.z; o[r4][7] = hi.w;
+        }
 #pragma unroll
-          for (int q = 0; q < 8; ++q) o[q] = o[q] * cur.sc[q] + cur.sh[q];
-          float r8[8];
-          if (p.res) {
+        for (int r4 = 0; r4 < 4; ++r4)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o[r4][q] = o[r4][q] * cur.sc[q] + cur.sh[q];
+        if (has_res && !res_post) {
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4) {
             const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&cur.rv[r4]);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const float2 f = __bfloat1622float2(rh[q]);
-              r8[2 * q] = f.x;
-              r8[2 * q + 1] = f.y;
-            }
-            if (!p.res_post) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] += r8[q];
+              o[r4][2 * q] += f.x;
+              o[r4][2 * q + 1] += f.y;
             }
           }
-          if (p.act == 1) {
+        }
+        if (act == 1) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
-          } else if (EPI == 1 && p.act == 2) {
+          for (int r4 = 0; r4 < 4; ++r4)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] *= fminf(fmaxf(o[q] + 3.f, 0.f), 6.f) * (1.f / 6.f);
-          } else if (EPI == 2 && p.act) {
+            for (int q = 0; q < 8; ++q) o[r4][q] = fmaxf(o[r4][q], 0.f);
+        } else if (EPI == 1 && act == 2) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = act_apply(o[q], p.act);
+          for (int r4 = 0; r4 < 4; ++r4)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              o[r4][q] *= fminf(fmaxf(o[r4][q] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+        } else if (EPI == 2 && act) {
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[r4][q] = act_apply(o[r4][q], act);
+        }
+        if (has_res && res_post) {
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4) {
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&cur.rv[r4]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __bfloat1622float2(rh[q]);
+              o[r4][2 * q] += f.x;
+              o[r4][2 * q + 1] += f.y;
+            }
           }
-          if (p.res && p.res_post) {
+        }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] += r8[q];
-          }
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const int m = m0 + rsub + 8 * r4;
+          if (m >= p.M) continue;
           const size_t off = static_cast<size_t>(m) * d.cout + col;
           if (!vec) {
-            store_ragged8(p.y, off, nv, p.out_f32, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
-          } else if (p.out_f32) {
+            store_ragged8(p.y, off, nv, out_f32, o[r4][0], o[r4][1], o[r4][2], o[r4][3], o[r4][4],
+                          o[r4][5], o[r4][6], o[r4][7]);
+          } else if (out_f32) {
             float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + off);
-            yp[0] = make_float4(o[0], o[1], o[2], o[3]);
-            yp[1] = make_float4(o[4], o[5], o[6], o[7]);
+            yp[0] = make_float4(o[r4][0], o[r4][1], o[r4][2], o[r4][3]);
+            yp[1] = make_float4(o[r4][4], o[r4][5], o[r4][6], o[r4][7]);
           } else {
             uint4 pk;
-            pk.x = pack_bf16x2(o[0], o[1]);
-            pk.y = pack_bf16x2(o[2], o[3]);
-            pk.z = pack_bf16x2(o[4], o[5]);
-            pk.w = pack_bf16x2(o[6], o[7]);
+            pk.x = pack_bf16x2(o[r4][0], o[r4][1]);
+            pk.y = pack_bf16x2(o[r4][2], o[r4][3]);
+            pk.z = pack_bf16x2(o[r4][4], o[r4][5]);
+            pk.w = pack_bf16x2(o[r4][6], o[r4][7]);
             *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + off) = pk;
           }
         }
       }
+      if (prof) w_wait2 += clock64() - tsec;
       __syncwarp();  // staging tile is rewritten by the next chunk
       cur = nxt;
       t = tn;
