@@ -27,7 +27,7 @@
 //    costs ~150-250 cycles, as much as four N=96 MMAs).
 //  * Accumulators live in a TMEM ring (NACC buffers of BN_MAX fp32 columns),
 //    so several tiles are in flight between MMA and epilogue.
-//  * Epilogue: two groups of 4 warps take alternate tiles; each warp
+//  * Epilogue: three groups of 4 warps stripe every tile's 32-column chunks; each warp
 //    tcgen05.ld's 32 TMEM lanes x 32 columns, transposes through padded smem,
 //    then applies SubnetNorm scale/shift, residual and the activation on
 //    coalesced 64-byte row segments and stores bf16 (or fp32 logits).
@@ -43,10 +43,11 @@ namespace ssn {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
-constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_EPI_WARPS = 12;  // 3 groups x 4 TMEM lane quarters
+constexpr int TC_EPI_GROUPS = TC_EPI_WARPS / 4;
 constexpr int TC_PROD_WARP = 0;
-constexpr int TC_MMA_WARP = 1 + TC_EPI_WARPS;       // 9
-constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 320
+constexpr int TC_MMA_WARP = 1 + TC_EPI_WARPS;       // 13
+constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 448
 constexpr int TC_STG_LD = 36;  // padded fp32 row of the 32x32 epilogue transpose tile
 constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
 
@@ -132,6 +133,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
   const int tiles = mt * nt;
   if (static_cast<int>(blockIdx.x) >= tiles) return;
+  // Epilogue work split: wide tiles (>= TC_EPI_GROUPS 32-column chunks) are
+  // striped chunk-wise across all groups; narrow ones go whole to one group
+  // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
+  const bool stripe = (bn + 31) / 32 >= TC_EPI_GROUPS;
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through shfl: the compiler then knows it is warp-uniform, so
   // role branches stay uniform and MMA/TMA operands live in uniform registers
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], TC_EPI_WARPS / 2);  // the 4 warps of the owning group
+      mbar_init(&tempty[a], stripe ? TC_EPI_WARPS : 4);  // warps that drain one tile
     }
     mbar_init(bfull, 1);
     fence_mbar_init();
@@ -250,13 +255,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // owns 8 consecutive columns of rows rsub, rsub+8, ... so residual loads
     // and output stores are 64-byte row-contiguous and coalesced (a
     // row-per-lane epilogue without the transpose measured 1.6x slower on the
-    // HBM-bound 1x1 convs).  Two groups (4 warps each, one per TMEM lane
-    // quarter) take alternate tiles.  Software-pipelined: the SubnetNorm row
-    // and residual of the NEXT chunk (possibly of the group's next tile) are
-    // in flight while this chunk is drained.
+    // HBM-bound 1x1 convs).  Three groups of 4 warps (one per TMEM lane
+    // quarter) split the work (see `stripe`).  Software-pipelined: the
+    // SubnetNorm row and residual of the warp's NEXT chunk are in flight
+    // while this chunk is drained.
     const int ew = warp - 1;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warps 1-4, 5-8)
-    const int group = ew >> 2;     // tile parity this warp drains
+    const int group = ew >> 2;     // chunk stripe this warp drains
     float* stg = epi_stage + ew * (32 * TC_STG_LD);
     const int seg = lane & 3, rsub = lane >> 2;
     const int nchunk = (bn + 31) / 32;
@@ -321,21 +326,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool res_post = p.res_post != 0;
     const int act = p.act;
     const bool out_f32 = p.out_f32 != 0;
-    int i = group;  // local tile ordinal
+    // Every tile is drained by all TC_EPI_GROUPS groups: group g takes the
+    // 32-column chunks c = g, g + G, ... (more warps in flight per tile than
+    // alternating whole tiles between two groups, which left the epilogue
+    // latency-bound).  A group without a chunk in a tile still waits for the
+    // accumulator and arrives on tempty (the barrier counts every warp).
+    const int i_step = stripe ? 1 : TC_EPI_GROUPS, c0 = stripe ? group : 0;
+    const int c_step = stripe ? TC_EPI_GROUPS : 1;
+    int i = stripe ? 0 : group;  // tile ordinal
     int t = blockIdx.x + i * static_cast<int>(gridDim.x);
-    int c = 0;
+    int c = c0;
     EpiIn cur, nxt;
-    if (t < tiles && !(p.dbg & 1)) fetch(cur, t, 0);
+    if (t < tiles && !(p.dbg & 1) && c < chunks_of(t)) fetch(cur, t, c);
     while (t < tiles) {
-      int tn = t, cn = c + 1, inx = i;
+      int tn = t, cn = c + c_step, inx = i;
       if (cn >= chunks_of(t)) {
-        cn = 0;
-        inx = i + 2;
-        tn = t + 2 * static_cast<int>(gridDim.x);
+        cn = c0;
+        inx = i + i_step;
+        tn = t + i_step * static_cast<int>(gridDim.x);
       }
-      if (tn < tiles && !(p.dbg & 1)) fetch(nxt, tn, cn);
+      if (tn < tiles && !(p.dbg & 1) && cn < chunks_of(tn)) fetch(nxt, tn, cn);
       const int a = i % NACC;
-      if (c == 0) {
+      if (c == c0) {
         if (prof) {
           const long long t0 = clock64();
           mbar_wait(&tfull[a], static_cast<uint32_t>(i / NACC) & 1);
@@ -344,6 +356,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&tfull[a], static_cast<uint32_t>(i / NACC) & 1);
         }
         tc_fence_after();
+      }
+      if (c >= chunks_of(t)) {  // no chunk of this tile for this group
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
+        cur = nxt;
+        t = tn;
+        c = cn;
+        i = inx;
+        continue;
       }
       const int m0 = (t / nt) * TC_BM + quarter * 32;
       const int cc = c * 32;
@@ -364,7 +386,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int q = 0; q < 8; ++q)
         srow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       __syncwarp();
-      if (cn == 0) {  // last chunk of this tile read out of TMEM: free the accumulator
+      if (inx != i) {  // this warp's last chunk of the tile is out of TMEM: free the accumulator
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
@@ -622,7 +644,7 @@ int choose_bn(int cout_max, long M) {
 // 36 KB epilogue staging fill the 227 KB of shared memory; resident-B
 // instances trade ring stages for the 96 KB weight block.
 #define SSN_TC_INSTANCES(X) X(64, 7, 1, 0) X(128, 5, 1, 0) X(256, 3, 1, 0) \
-  X(64, 5, 1, 1) X(128, 5, 1, 1) X(256, 5, 1, 1)
+  X(64, 4, 1, 1) X(128, 4, 1, 1) X(256, 4, 1, 1)
 
 cudaError_t init_conv_tc() {
 #define SSN_TC_ATTR(BN, ST, KPS, RB)                                                      \
@@ -666,10 +688,10 @@ cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cuda
   // all its K blocks fit TC_RB_BYTES.
   const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
   const bool resb = !(p.dbg & 512) && p.cout_max <= p.bn && nk_max * p.bn * TC_BK * 2 <= TC_RB_BYTES;
-  if (p.bn <= 64) return resb ? launch_impl<64, 5, 1, 1>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
+  if (p.bn <= 64) return resb ? launch_impl<64, 4, 1, 1>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
   if (p.bn <= 128)
-    return resb ? launch_impl<128, 5, 1, 1>(p, wmap, s) : launch_impl<128, 5, 1, 0>(p, wmap, s);
-  return resb ? launch_impl<256, 5, 1, 1>(p, wmap, s) : launch_impl<256, 3, 1, 0>(p, wmap, s);
+    return resb ? launch_impl<128, 4, 1, 1>(p, wmap, s) : launch_impl<128, 5, 1, 0>(p, wmap, s);
+  return resb ? launch_impl<256, 4, 1, 1>(p, wmap, s) : launch_impl<256, 3, 1, 0>(p, wmap, s);
 }
 
 }  // namespace ssn
