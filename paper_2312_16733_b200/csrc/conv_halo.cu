@@ -24,7 +24,7 @@
 // Garbage positions (the k-1 padding columns of each row, rows past H) are
 // computed and dropped by the epilogue (3.4% of MMA work at 56 px).
 // Warp roles as conv_tc: warp 0 TMA producer, warp 9 MMA issuer (one
-// elected lane), warps 1-8 epilogue in two groups of 4 taking alternate
+// elected lane), warps 1-12 epilogue in three groups of 4 taking alternate
 // tiles; accumulators in a TMEM ring.  The epilogue is row-per-lane (no
 // smem staging: shared memory belongs to the resident weights).
 #include <cstdio>
@@ -34,7 +34,8 @@
 
 namespace ssn {
 
-constexpr int HL_EPI_WARPS = 8;
+constexpr int HL_EPI_WARPS = 12;  // 3 groups x 4 TMEM lane quarters
+constexpr int HL_EPI_GROUPS = HL_EPI_WARPS / 4;
 constexpr int HL_MMA_WARP = 1 + HL_EPI_WARPS;
 constexpr int HL_THREADS = (HL_MMA_WARP + 1) * 32;
 constexpr int HL_SMEM_MAX = 232448;  // 227 KB opt-in
@@ -59,12 +60,18 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   const int acc_cols = bn <= 128 ? 128 : 256;
   const int nacc = 512 / acc_cols > 4 ? 4 : 512 / acc_cols;
 
-  // shared memory: [resident B][A ring][barriers]
-  const uint32_t b_chunk = static_cast<uint32_t>(p.hb_rows) * 16;      // K-chunk stride in B
-  const uint32_t b_tap = b_chunk * static_cast<uint32_t>(p.hb_chunks);  // tap stride in B
-  const uint32_t b_bytes = b_tap * static_cast<uint32_t>(ka * ka);
-  const uint32_t a_chunk = static_cast<uint32_t>(R * wp) * 16;         // K-chunk stride in A
-  const uint32_t a_stage = (a_chunk * (HL_CB / 8) + 127) & ~127u;  // TMA dst: 128-B aligned
+  // shared memory: [resident B][A ring][barriers].  Both operands are
+  // 64B-swizzled K-major: rows of 32 channels (64 B), 8-row atoms of 512 B.
+  // B block (tap, 32-ch block cb) = hb_rows rows; an A stage = one halo
+  // window of R * Wp pixel rows for one 32-channel block.  A tap's A operand
+  // starts (r*Wp + s) rows into the window: the tensor core applies the
+  // swizzle on absolute smem address bits, so any 64-B row offset is a legal
+  // start (verified exact on B200: tools/ubench/sw128_shift.cu -DSW64).
+  const int ncb_max = p.hb_chunks;                                      // 32-ch blocks (max shape)
+  const uint32_t b_blk = static_cast<uint32_t>(p.hb_rows) * 64;        // one (tap, cb) block
+  const uint32_t b_bytes = b_blk * static_cast<uint32_t>(ka * ka * ncb_max);
+  const uint32_t a_box = static_cast<uint32_t>(R * wp) * 64;           // TMA box bytes
+  const uint32_t a_stage = (a_box + 1023) & ~1023u;                    // swizzle-atom aligned
   const int ST = p.h_stages;
   uint8_t* sB = smem;
   uint8_t* sA = smem + ((b_bytes + 1023) & ~1023u);
@@ -87,7 +94,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     }
     for (int a = 0; a < 4; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], HL_EPI_WARPS / 2);
+      mbar_init(&tempty[a], 4);  // the owning group's warps
     }
     mbar_init(bfull, 1);
     fence_mbar_init();
@@ -118,13 +125,14 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     if (leader && (p.dbg & 8)) {  // profiling: no weight load
       mbar_arrive(bfull);
     } else if (leader) {
-      // the active k_a x k_a centre crop of the max-shape weights, all cin/cout
-      // chunks of the max shape (channels past cin_a meet zero-filled A)
+      // the active k_a x k_a centre crop of the max-shape weights, all 32-ch
+      // blocks of the max shape (channels past cin_a meet zero-filled A)
       mbar_arrive_expect_tx(bfull, b_bytes);
       for (int r = 0; r < ka; ++r)
         for (int s = 0; s < ka; ++s)
-          tma_load_4d(sB + (r * ka + s) * b_tap, &wmap, bfull, 0, 0, 0,
-                      (r + koff) * p.k_max + (s + koff));
+          for (int cb = 0; cb < ncb_max; ++cb)
+            tma_load_3d(sB + ((r * ka + s) * ncb_max + cb) * b_blk, &wmap, bfull, cb * HL_CB,
+                        (r + koff) * p.k_max + (s + koff), 0);
     }
     const CUtensorMap* amap = &dp->amap;
     int g = 0;
@@ -138,8 +146,8 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
           if (p.dbg & 4) {  // profiling: no A loads
             mbar_arrive(&full[s]);
           } else {
-            mbar_arrive_expect_tx(&full[s], a_chunk * (HL_CB / 8));  // box bytes (stage is padded)
-            tma_load_5d(sA + s * a_stage, amap, &full[s], 0, -pad, r0 - pad, img, cb * (HL_CB / 8));
+            mbar_arrive_expect_tx(&full[s], a_box);  // box bytes (the stage is padded)
+            tma_load_4d(sA + s * a_stage, amap, &full[s], cb * HL_CB, -pad, r0 - pad, img);
           }
         }
         __syncwarp();
@@ -150,10 +158,11 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     // Converged warp, elected lane issues (tc_mma_bf16_elect); descriptors
     // are a per-stage / per-block base plus 16-byte-unit offsets.
     const uint32_t idesc = umma_idesc_bf16(bn);
-    const uint64_t a_base = umma_desc_noswz(smem_u32(sA), a_chunk, 128);
-    const uint64_t b_base = umma_desc_noswz(smem_u32(sB), b_chunk, 128);
-    const uint32_t a_st16 = a_stage >> 4, a_ks16 = (2 * a_chunk) >> 4;
-    const uint32_t b_tap16 = b_tap >> 4, b_ks16 = (2 * b_chunk) >> 4, b_cb16 = ((HL_CB / 8) * b_chunk) >> 4;
+    const uint64_t a_base = umma_desc_sw64(smem_u32(sA));
+    const uint64_t b_base = umma_desc_sw64(smem_u32(sB));
+    const uint32_t a_st16 = a_stage >> 4;
+    const uint32_t b_tap16 = (ncb_max * b_blk) >> 4, b_cb16 = b_blk >> 4;
+    constexpr uint32_t ks16 = 2;  // K=16 step inside a 64-B row: +32 B
     HL_WAIT(w_wait, bfull, 0);
     tc_fence_after();
     int g = 0, i = 0;
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         tc_fence_after();
         const int nks = min(HL_CB / 16, (cin16 - cb * HL_CB) / 16);
         const uint64_t ad = a_base + static_cast<uint64_t>(s * a_st16);
-        const uint64_t bd = b_base + static_cast<uint64_t>(cb * b_cb16);
+        const uint64_t bd = b_base + static_cast<uint64_t>(cb * b_cb16);  // + tap * b_tap16 below
         if (p.dbg & 2) {  // profiling: no MMAs
         } else if (ka == 3 && nks == 2) {  // OFA-R50: fully unrolled 3x3 taps, full block
 #pragma unroll
@@ -177,15 +186,15 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
             for (int c = 0; c < 3; ++c)
 #pragma unroll
               for (int j = 0; j < 2; ++j)
-                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(r * wp + c + j * a_ks16),
-                                  bd + static_cast<uint64_t>((r * 3 + c) * b_tap16 + j * b_ks16),
+                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>((r * wp + c) * 4 + j * ks16),
+                                  bd + static_cast<uint64_t>((r * 3 + c) * b_tap16 + j * ks16),
                                   idesc, (cb | r | c | j) != 0 ? 1u : 0u);
         } else {
           for (int r = 0; r < ka; ++r)
             for (int c = 0; c < ka; ++c)
               for (int j = 0; j < nks; ++j)
-                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(r * wp + c + j * a_ks16),
-                                  bd + static_cast<uint64_t>((r * ka + c) * b_tap16 + j * b_ks16),
+                tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>((r * wp + c) * 4 + j * ks16),
+                                  bd + static_cast<uint64_t>((r * ka + c) * b_tap16 + j * ks16),
                                   idesc, (cb | r | c | j) != 0 ? 1u : 0u);
         }
         tc_commit_elect(&empty[s]);
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     const int nch = (d.cout + 31) / 32;
     int i = group;
     for (int t = blockIdx.x + group * static_cast<int>(gridDim.x); t < tiles;
-         t += 2 * static_cast<int>(gridDim.x), i += 2) {
+         t += HL_EPI_GROUPS * static_cast<int>(gridDim.x), i += HL_EPI_GROUPS) {
       const int a = i % nacc;
       const int img = t / tpi;
       const int oh = (t - img * tpi) * rt + oh_l;
@@ -322,13 +331,13 @@ static EncodeTiledFnH tiled_encoder() {
 }
 
 static int halo_b_rows(int cout_max) { return (cout_max + 15) / 16 * 16; }
-static int halo_b_chunks(int cin_max) { return (cin_max + 15) / 16 * 2; }
+static int halo_b_chunks(int cin_max) { return (cin_max + HL_CB - 1) / HL_CB; }  // 32-ch blocks
 
 // Resident-B and ring sizing for an op's MAX shape (every subnet fits in it).
 static void halo_sizes(int w, int k_max, int cin_max, int cout_max, long* b_bytes, long* a_stage) {
   const HaloGeom g = halo_geom(w, k_max);
-  *b_bytes = static_cast<long>(k_max) * k_max * halo_b_chunks(cin_max) * halo_b_rows(cout_max) * 16;
-  *a_stage = (static_cast<long>(g.r) * g.wp * 16 * (HL_CB / 8) + 127) & ~127L;
+  *b_bytes = static_cast<long>(k_max) * k_max * halo_b_chunks(cin_max) * halo_b_rows(cout_max) * 64;
+  *a_stage = (static_cast<long>(g.r) * g.wp * 64 + 1023) & ~1023L;
 }
 
 static int halo_stages(int w, int k_max, int cin_max, int cout_max) {
@@ -354,40 +363,38 @@ bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_ma
   return halo_stages(w, k_max, cin_max, cout_max) >= 2;
 }
 
-// A operand: [n][h][w][cin] NHWC bf16 viewed as (c8, w, h, n, c/8) so the box
-// {8, Wp, R, 1, 4} lands as [chunk][row][col][8]: 4 K-chunks of the halo
-// window, pixel rows 16 bytes apart (no-swizzle K-major core matrices).
+// A operand: [n][h][w][cin_a] NHWC bf16, box {32 ch, Wp, R, 1} with 64-byte
+// swizzle: one halo window of one 32-channel block as 64-B pixel rows.
 int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k) {
   EncodeTiledFnH enc = tiled_encoder();
   if (!enc) return -1;
   const HaloGeom g = halo_geom(w, k);
-  cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
-                        static_cast<cuuint64_t>(n), static_cast<cuuint64_t>((cin + 7) / 8)};
-  cuuint64_t strides[4] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(w) * cin * 2,
-                           static_cast<cuuint64_t>(h) * w * cin * 2, 16};
-  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(g.wp), static_cast<cuuint32_t>(g.r), 1,
-                       HL_CB / 8};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
+                        static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(w) * cin * 2,
+                           static_cast<cuuint64_t>(h) * w * cin * 2};
+  cuuint32_t box[4] = {HL_CB, static_cast<cuuint32_t>(g.wp), static_cast<cuuint32_t>(g.r), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
 }
 
-// B operand: max-shape KRSC [cout][taps][cin_store] viewed as (c8, n, c/8, tap);
-// one box {8, rows, chunks, 1} per tap lands as [chunk][n][8].
+// B operand: max-shape KRSC [cout][taps][cin_store], box {32 ch, 1 tap, rows}
+// with 64-byte swizzle: one (tap, 32-channel block) of the weight slice.
 static int make_halo_weight_map(CUtensorMap* map, const void* wgt, int cin_store, int taps,
-                                int cout, int rows, int chunks) {
+                                int cout, int rows, int /*chunks*/) {
   EncodeTiledFnH enc = tiled_encoder();
   if (!enc) return -1;
-  cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(cout),
-                        static_cast<cuuint64_t>((cin_store + 7) / 8), static_cast<cuuint64_t>(taps)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(taps) * cin_store * 2, 16,
-                           static_cast<cuuint64_t>(cin_store) * 2};
-  cuuint32_t box[4] = {8, static_cast<cuuint32_t>(rows), static_cast<cuuint32_t>(chunks), 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(wgt), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin_store), static_cast<cuuint64_t>(taps),
+                        static_cast<cuuint64_t>(cout)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cin_store) * 2,
+                           static_cast<cuuint64_t>(taps) * cin_store * 2};
+  cuuint32_t box[3] = {HL_CB, 1, static_cast<cuuint32_t>(rows)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(wgt), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
 }

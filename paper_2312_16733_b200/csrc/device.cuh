@@ -407,6 +407,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B: 64-byte rows (32 bf16),
+// 8-row atoms 512 B apart (SBO); K step of 16 = +32 B (+2 in the address field).
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>(16 >> 4) << 16;   // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(512 >> 4) << 32;  // SBO
+  d |= static_cast<uint64_t>(1) << 46;         // version
+  d |= static_cast<uint64_t>(4) << 61;         // SWIZZLE_64B
+  return d;
+}
+
 // UMMA shared-memory descriptor: K-major, no swizzle ("interleave"): 8-row x
 // 16-byte core matrices, N-adjacent core matrices `sbo` bytes apart,
 // K-adjacent ones `lbo` bytes apart.
