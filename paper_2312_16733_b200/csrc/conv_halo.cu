@@ -56,9 +56,12 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   if (static_cast<int>(blockIdx.x) >= tiles) return;
   const int cin16 = (d.cin + 15) & ~15;
   const int ncb = (cin16 + HL_CB - 1) / HL_CB;
-  const int bn = (d.cout + 15) & ~15;  // MMA N: the whole active cout (<= 256)
-  const int acc_cols = bn <= 128 ? 128 : 256;
-  const int nacc = 512 / acc_cols > 4 ? 4 : 512 / acc_cols;
+  const int bn = (d.cout + 15) & ~15;  // MMA N: the whole active cout (<= 128)
+  // 3 accumulators of 128 columns: the 3 epilogue groups take tiles in
+  // turn, so accumulator a is always drained by group a (a group never waits
+  // on an mbarrier phase belonging to an older use of another group's tile)
+  const int acc_cols = 128;
+  const int nacc = HL_EPI_GROUPS;
 
   // shared memory: [resident B][A ring][barriers].  Both operands are
   // 64B-swizzled K-major: rows of 32 channels (64 B), 8-row atoms of 512 B.
@@ -356,7 +359,7 @@ bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_ma
     return e && atoi(e) != 0;
   }();
   if (off) return false;
-  if (stride != 1 || (k_max & 1) == 0 || k_max < 3 || cout_max > 256) return false;
+  if (stride != 1 || (k_max & 1) == 0 || k_max < 3 || cout_max > 128) return false;
   if (w < 14 || h < 2) return false;
   const HaloGeom g = halo_geom(w, k_max);
   if (g.wp > 256 || g.r > 256) return false;

@@ -66,7 +66,11 @@ struct TcCfg {
   static constexpr int STAGE_BYTES = KPS * (A_BYTES + (RESB ? 0 : B_BYTES));
   // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
   // (max 4), so the MMA can run several tiles ahead of the epilogue.
-  static constexpr int NACC = 512 / BN_MAX > 4 ? 4 : 512 / BN_MAX;
+  // (BN_MAX 64 -> 3: narrow tiles alternate whole across the 3 epilogue
+  // groups, and each accumulator must always be drained by the same group,
+  // else a group could pass a stale mbarrier phase of an older use.)
+  static constexpr int NACC = BN_MAX <= 64 ? 3 : (512 / BN_MAX > 4 ? 4 : 512 / BN_MAX);
+  static constexpr int TMEM_COLS = NACC * BN_MAX <= 256 ? 256 : 512;  // power-of-2 allocation
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + (RESB ? TC_RB_BYTES : 0) +
                               TC_STG_BYTES + (2 * STAGES + 2 * NACC + 1) * 8 + 16;
   static_assert(SMEM <= 232448, "operand ring exceeds 227 KB of shared memory");
@@ -137,6 +141,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // striped chunk-wise across all groups; narrow ones go whole to one group
   // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
   const bool stripe = (bn + 31) / 32 >= TC_EPI_GROUPS;
+  // alternate mode hands tile i to group i % 3 and accumulator i % NACC: the
+  // pair must be a function of the accumulator alone
+  static_assert(BN_MAX > 64 || C::NACC % TC_EPI_GROUPS == 0, "accumulator/group mapping");
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through shfl: the compiler then knows it is warp-uniform, so
   // role branches stay uniform and MMA/TMA operands live in uniform registers
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch(&wmap);
     tma_prefetch(&dp->amap);
   }
-  if (warp == TC_MMA_WARP) tmem_alloc(tmem_slot, NACC * BN_MAX);
+  if (warp == TC_MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == TC_MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem, NACC * BN_MAX);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
