@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool leader = elect_one();
     const CUtensorMap* amap = &dp->amap;
     const int hwo = p.ho * p.wo;
+    const bool pointwise = p.k_max == 1 && p.stride == 1;  // A map is 2-D tiled (make_act_map)
     const uint32_t kb_bytes = static_cast<uint32_t>(C::A_BYTES + (RESB ? 0 : bn * TC_BK * 2));
     if (RESB && leader) {
       // the whole (single-N-tile) weight slice, once per CTA: block kb = (tap, channel block)
@@ -235,9 +236,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < KPS; ++j) {
           if (j < nsub) {
             if (leader) {
-              if (!(p.dbg & 4))
+              if (p.dbg & 4) {
+              } else if (pointwise) {  // 1x1 stride 1: plain 2-D tile of the [M][cin_a] matrix
+                tma_load_2d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, m0);
+              } else {
                 tma_im2col_4d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0,
                               img, static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
+              }
               if (!RESB && !(p.dbg & 8))
                 tma_load_3d(sB + (s * KPS + j) * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
                             (tr + koff) * p.k_max + (ts + koff), n0);
@@ -597,6 +602,20 @@ int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, in
 // for a k x k / stride / pad convolution: 128 pixels x 64 channels per load.
 int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
                  int pad) {
+  if (k == 1 && stride == 1 && pad == 0) {
+    // pointwise conv: the activation is a plain [n*h*w][cin] matrix; a tiled
+    // box {64 ch, 128 rows} is cheaper for the TMA unit than im2col mode
+    static EncodeTiledFn tenc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
+    if (!tenc) return -1;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(n) * h * w};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cin) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(TC_BK), static_cast<cuuint32_t>(TC_BM)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = tenc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
+  }
   static EncodeIm2colFn enc = driver_fn<EncodeIm2colFn>("cuTensorMapEncodeIm2col");
   if (!enc) return -1;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
