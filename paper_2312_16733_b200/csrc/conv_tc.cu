@@ -45,9 +45,19 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
 constexpr int TC_EPI_WARPS = 12;  // 3 groups x 4 TMEM lane quarters
 constexpr int TC_EPI_GROUPS = TC_EPI_WARPS / 4;
+// Warp roles.  Warpgroup 0 = warp 0 A producer, warp 1 MMA issuer, warp 2 B
+// producer (warp 3 idle); warpgroups 1-3 = the 12 epilogue warps.  One
+// thread sustains only ~1 TMA box per ~360 cycles (wait + expect_tx + issue;
+// tools/ubench/tma_rate.cu: 45 B/cycle with 16 KB boxes from one thread, 76
+// with two), less than a K block of N=128 MMAs, so A and B have separate
+// issuers.  512 threads cap registers at 128: the epilogue keeps no
+// register prefetch of the next chunk.
 constexpr int TC_PROD_WARP = 0;
-constexpr int TC_MMA_WARP = 1 + TC_EPI_WARPS;       // 13
-constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 448
+constexpr int TC_MMA_WARP = 1;
+constexpr int TC_PROD2_WARP = 2;
+constexpr int TC_EPI_WARP0 = 4;
+constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 512
+
 constexpr int TC_STG_LD = 36;  // padded fp32 row of the 32x32 epilogue transpose tile
 constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
 
@@ -155,7 +165,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);  // the producer's expect_tx arrival
+      mbar_init(&full[s], RESB ? 1 : 2);  // the A (and B) producers' expect_tx arrivals
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
@@ -177,14 +187,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   long long w_wait = 0, w_wait2 = 0;
   const long long t_begin = prof ? clock64() : 0;
 
-  if (warp == TC_PROD_WARP) {
-    // ============================================================ producer
+  if (warp == TC_PROD_WARP || (warp == TC_PROD2_WARP && !RESB)) {
+    // ============================================================ producers
+    // warp 0: A (activations) + the resident-B preload; warp 14: B (weights)
+    const bool role_b = warp == TC_PROD2_WARP;
     const bool leader = elect_one();
     const CUtensorMap* amap = &dp->amap;
     const int hwo = p.ho * p.wo;
     const bool pointwise = p.k_max == 1 && p.stride == 1;  // A map is 2-D tiled (make_act_map)
-    const uint32_t kb_bytes = static_cast<uint32_t>(C::A_BYTES + (RESB ? 0 : bn * TC_BK * 2));
-    if (RESB && leader) {
+    if (RESB && leader && !role_b) {
       // the whole (single-N-tile) weight slice, once per CTA: block kb = (tap, channel block)
       if (p.dbg & 8) {
         mbar_arrive(bfull);
@@ -227,15 +238,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int nsub = min(KPS, nk - kb);
         if (leader) {
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES);
-          const uint32_t b_tx = ((p.dbg & 8) || RESB) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
-          const uint32_t tx = (p.dbg & 12) ? nsub * (a_tx + b_tx) : nsub * kb_bytes;
+          const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
+          const uint32_t tx = nsub * (role_b ? b_tx : a_tx);
           if (tx) mbar_arrive_expect_tx(&full[s], tx);
           else mbar_arrive(&full[s]);
         }
 #pragma unroll
         for (int j = 0; j < KPS; ++j) {
           if (j < nsub) {
-            if (leader) {
+            if (leader && !role_b) {
               if (p.dbg & 4) {
               } else if (pointwise) {  // 1x1 stride 1: plain 2-D tile of the [M][cin_a] matrix
                 tma_load_2d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, m0);
@@ -243,10 +254,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tma_im2col_4d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0,
                               img, static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
               }
-              if (!RESB && !(p.dbg & 8))
-                tma_load_3d(sB + (s * KPS + j) * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
-                            (tr + koff) * p.k_max + (ts + koff), n0);
             }
+            if (leader && role_b && !(p.dbg & 8))
+              tma_load_3d(sB + (s * KPS + j) * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
+                          (tr + koff) * p.k_max + (ts + koff), n0);
             if (++cb == cblocks) {
               cb = 0;
               if (++ts == ka) {
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
       }
     }
-  } else if (warp < TC_MMA_WARP) {
+  } else if (warp >= TC_EPI_WARP0) {
     // ============================================================ epilogue
     // TMEM gives each thread one ROW; global memory wants each warp to touch
     // whole row segments.  Each 32x32 fp32 chunk is transposed through a
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // quarter) split the work (see `stripe`).  Software-pipelined: the
     // SubnetNorm row and residual of the warp's NEXT chunk are in flight
     // while this chunk is drained.
-    const int ew = warp - 1;
+    const int ew = warp - TC_EPI_WARP0;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warps 1-4, 5-8)
     const int group = ew >> 2;     // chunk stripe this warp drains
     float* stg = epi_stage + ew * (32 * TC_STG_LD);
@@ -348,8 +359,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int i = stripe ? 0 : group;  // tile ordinal
     int t = blockIdx.x + i * static_cast<int>(gridDim.x);
     int c = c0;
-    EpiIn cur, nxt;
-    if (t < tiles && !(p.dbg & 1) && c < chunks_of(t)) fetch(cur, t, c);
+    EpiIn cur;  // this chunk's SubnetNorm row + residual (no register prefetch:
+                // 12 warps hide the latency, and 512 threads cap registers at 128)
     while (t < tiles) {
       int tn = t, cn = c + c_step, inx = i;
       if (cn >= chunks_of(t)) {
@@ -357,7 +368,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         inx = i + i_step;
         tn = t + i_step * static_cast<int>(gridDim.x);
       }
-      if (tn < tiles && !(p.dbg & 1) && cn < chunks_of(tn)) fetch(nxt, tn, cn);
+      // operands of this chunk, issued before the accumulator wait / TMEM load
+      if (!(p.dbg & 1) && c < chunks_of(t)) fetch(cur, t, c);
       const int a = i % NACC;
       if (c == c0) {
         if (prof) {
@@ -373,7 +385,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
-        cur = nxt;
         t = tn;
         c = cn;
         i = inx;
@@ -486,12 +497,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (prof) w_wait2 += clock64() - tsec;
       __syncwarp();  // staging tile is rewritten by the next chunk
-      cur = nxt;
       t = tn;
       c = cn;
       i = inx;
     }
-  } else {
+  } else if (warp == TC_MMA_WARP) {
     // ============================================================ MMA issuer
     // Converged warp, elected lane issues (tc_mma_bf16_elect); descriptors
     // are a base plus 16-byte-unit offsets (SW128: K step = +32 B).
@@ -547,7 +557,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   }
-  if (prof && lane == 0 && (warp == TC_PROD_WARP || warp == TC_MMA_WARP || warp == 1))
+  if (prof && lane == 0 && (warp == TC_PROD_WARP || warp == TC_MMA_WARP || warp == TC_EPI_WARP0))
     printf("[conv_tc prof] tiles=%d nk=%d warp=%d total=%lld wait=%lld wait2=%lld\n", tiles, nk, warp,
            clock64() - t_begin, w_wait, w_wait2);
   tc_fence_before();

@@ -1,0 +1,93 @@
+// TMA L2->smem feed rate per SM: every CTA (one per SM) streams boxes of an
+// L2-resident bf16 matrix through a STAGES-deep ring; a consumer warp only
+// waits and releases.  Reports bytes per SM-cycle (profiling aid).
+#include <cstdio>
+#include <cuda.h>
+#include "device.cuh"
+using namespace ssn;
+
+template <int STAGES, int BOX_ROWS, int P>
+__global__ void __launch_bounds__(256, 1) k(const __grid_constant__ CUtensorMap map, int iters, int rows_total,
+                                          long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* buf = sm;
+  constexpr int BYTES = BOX_ROWS * 128;
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  if (warp < P && lane == 0) {  // P producer warps, each owning stages s = warp (mod P)
+    for (int g = warp; g < iters; g += P) {
+      const int s = g % STAGES;
+      mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], BYTES);
+      const int row = ((blockIdx.x * 7 + g) * BOX_ROWS) % rows_total;
+      tma_load_2d(buf + s * BYTES, &map, &full[s], 0, row);
+    }
+  } else if (warp == P && lane == 0) {
+    for (int g = 0; g < iters; ++g) {
+      const int s = g % STAGES;
+      mbar_wait(&full[s], (g / STAGES) & 1);
+      mbar_arrive(&empty[s]);
+    }
+    out[blockIdx.x] = clock64() - t0;
+  }
+}
+
+template <int STAGES, int BOX_ROWS, int P>
+void run(CUtensorMap map, int rows_total, long long* d) {
+  const int iters = 2000;
+  const int smem = STAGES * BOX_ROWS * 128 + 1024;
+  cudaFuncSetAttribute(k<STAGES, BOX_ROWS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int rep = 0; rep < 2; ++rep) k<STAGES, BOX_ROWS, P><<<148, 256, smem>>>(map, iters, rows_total, d);
+  cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double mx = 0;
+  for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+  printf("producers=%d stages=%2d box=%3d rows (%5d B): %6.1f B/cycle/SM (slowest SM)\n", P, STAGES,
+         BOX_ROWS, BOX_ROWS * 128, double(iters) * BOX_ROWS * 128 / mx);
+}
+
+int main() {
+  const int rows = 16384;  // 16384 x 64 bf16 = 2 MB: L2 resident
+  void* src;
+  cudaMalloc(&src, rows * 128);
+  cudaMemset(src, 0, rows * 128);
+  long long* d;
+  cudaMalloc(&d, 148 * 8);
+  using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  Enc enc = reinterpret_cast<Enc>(fn);
+  auto mk = [&](int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return m;
+  };
+  run<8, 64, 1>(mk(64), rows, d);
+  run<8, 128, 1>(mk(128), rows, d);
+  run<6, 256, 1>(mk(256), rows, d);
+  run<8, 64, 2>(mk(64), rows, d);
+  run<8, 128, 2>(mk(128), rows, d);
+  run<6, 256, 2>(mk(256), rows, d);
+  run<8, 128, 4>(mk(128), rows, d);
+  run<8, 256, 4>(mk(256), rows, d);
+  return 0;
+}
