@@ -6,6 +6,8 @@
 // the actuated subnet's OpDesc (device memory), so the same graph-captured
 // launch serves every subnet.  bf16 paths move 8 channels (16 B) per thread
 // access; active widths are multiples of 8 (OFA make_divisible(., 8)).
+#include <algorithm>
+
 #include "../../include/ssn.h"
 #include "device.cuh"
 
@@ -49,6 +51,57 @@ __global__ void input_kernel(InputParams p) {
 // Input staging fused with the stem conv's im2col (bf16): output pixel
 // (n, oh, ow) gets the k*k*3 input values (r, s, c) of its window, zero
 // padded, then zeros up to cpad (a multiple of 8) — a K = cpad GEMM operand.
+// k = 3, cpad = 32 (both OFA stems): the 27 window values of one output
+// pixel live in registers (the generic kernel below indexes a local array)
+// and leave as four 16-byte stores.
+template <bool U8>
+__global__ void __launch_bounds__(256) input_im2col3_kernel(InputParams p) {
+  const long npix = static_cast<long>(p.n) * p.ho * p.wo;
+  const int st = p.im2col_stride;
+  const long hw = static_cast<long>(p.h) * p.w;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < npix;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long hwo = static_cast<long>(p.ho) * p.wo;
+    const long img = i / hwo;
+    const int rem = static_cast<int>(i - img * hwo);
+    const int oh = rem / p.wo, ow = rem - oh * p.wo;
+    float v[32];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int ih = oh * st - 1 + r;
+      const bool rok = ih >= 0 && ih < p.h;
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) {
+        const int iw = ow * st - 1 + s2;
+        const bool ok = rok && iw >= 0 && iw < p.w;
+        const int base = (r * 3 + s2) * 3;
+        if (U8) {
+          const uint8_t* src = static_cast<const uint8_t*>(p.raw) + ((img * p.h + ih) * p.w + iw) * 3;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            v[base + c] = ok ? (static_cast<float>(__ldg(src + c)) - 128.f) * (1.f / 64.f) : 0.f;
+        } else {
+          const float* src = static_cast<const float*>(p.raw) + img * 3 * hw + static_cast<long>(ih) * p.w + iw;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) v[base + c] = ok ? __ldg(src + c * hw) : 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 27; q < 32; ++q) v[q] = 0.f;
+    uint4* y = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + i * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16x2(v[8 * q], v[8 * q + 1]);
+      u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+      u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+      u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+      y[q] = u;
+    }
+  }
+}
+
 __global__ void input_im2col_kernel(InputParams p) {
   const long npix = static_cast<long>(p.n) * p.ho * p.wo;
   const int k = p.im2col_k, st = p.im2col_stride, pad = k / 2;
@@ -115,6 +168,40 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
   u.z = pack_bf16x2(f[4], f[5]);
   u.w = pack_bf16x2(f[6], f[7]);
   return u;
+}
+
+// Global average pool, bf16 [n][hw][C] -> [n][C]: block (image, 64-channel
+// chunk), 8 channel groups x 32 pixel lanes and a shared-memory reduction,
+// so the hw loads of a channel group are in flight together (one thread per
+// channel group summing hw pixels serially was latency-bound).
+__global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin;
+  const int n = blockIdx.x, c0 = blockIdx.y * 64;
+  if (c0 >= C) return;
+  const int hw = p.h * p.w;
+  const int g = threadIdx.x & 7, lane = threadIdx.x >> 3;
+  const int c = c0 + g * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * hw * C;
+  if (c < C) {
+    for (int q = lane; q < hw; q += 32) {
+      float f[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * C + c)), f);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] += f[t];
+    }
+  }
+  __shared__ float red[32][65];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) red[lane][g * 8 + t] = acc[t];
+  __syncthreads();
+  if (threadIdx.x < 64 && c0 + threadIdx.x < C) {
+    float sum = 0.f;
+    for (int l = 0; l < 32; ++l) sum += red[l][threadIdx.x];
+    static_cast<__nv_bfloat16*>(p.y)[static_cast<long>(n) * C + c0 + threadIdx.x] =
+        __float2bfloat16_rn(sum / static_cast<float>(hw));
+  }
 }
 
 __global__ void pool_bf16_kernel(PoolParams p) {
@@ -580,8 +667,16 @@ static inline int grid_for(long work, int block) {
 }
 
 cudaError_t launch_input(const InputParams& p, cudaStream_t s) {
-  if (p.im2col_k > 0)
-    input_im2col_kernel<<<grid_for(static_cast<long>(p.n) * p.ho * p.wo, 128), 128, 0, s>>>(p);
+  const long npix = static_cast<long>(p.n) * p.ho * p.wo;
+  if (p.im2col_k == 3 && p.cpad == 32) {
+    const int grid = static_cast<int>(std::min<long>((npix + 255) / 256, 148L * 8));
+    if (p.format == SSN_INPUT_U8_NHWC)
+      input_im2col3_kernel<true><<<grid, 256, 0, s>>>(p);
+    else
+      input_im2col3_kernel<false><<<grid, 256, 0, s>>>(p);
+  } else if (p.im2col_k > 0) {
+    input_im2col_kernel<<<grid_for(npix, 128), 128, 0, s>>>(p);
+  }
   else
     input_kernel<<<grid_for(static_cast<long>(p.n) * p.h * p.w, 256), 256, 0, s>>>(p);
   return cudaGetLastError();
@@ -592,7 +687,9 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
   const long per = bf16 ? max_c / 8 : max_c;
   const long work = p.kind == 4 ? static_cast<long>(p.n) * per
                                 : static_cast<long>(p.n) * p.ho * p.wo * per;
-  if (bf16)
+  if (bf16 && p.kind == 4)
+    gap_bf16_kernel<<<dim3(p.n, (max_c + 63) / 64), 256, 0, s>>>(p);
+  else if (bf16)
     pool_bf16_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
   else
     pool_f32_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
