@@ -204,6 +204,55 @@ __global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
   }
 }
 
+// Max (KIND 2) / ceil-average (KIND 3) pooling with a compile-time window:
+// grid (output rows n*ho, ceil(wo * C/8 / 256)); all K*K 16-byte loads of a
+// thread are independent and issued together (the generic kernel's runtime
+// window loop serialised them), 32-bit index math.
+template <int K, int KIND>
+__global__ void __launch_bounds__(256) pool_k_bf16_kernel(PoolParams p) {
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const int C = d.cin, G = C >> 3;
+  const int row = blockIdx.y;
+  const int img = row / p.ho, oh = row - img * p.ho;
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= p.wo * G) return;
+  const int ow = j / G, g = j - ow * G;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + g * 8;
+  uint4 v[K * K];
+  bool ok[K * K];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int s2 = 0; s2 < K; ++s2) {
+      const int ih = oh * p.stride - p.pad + r, iw = ow * p.stride - p.pad + s2;
+      ok[r * K + s2] = ih >= 0 && ih < p.h && iw >= 0 && iw < p.w;
+      v[r * K + s2] = ok[r * K + s2]
+                          ? __ldg(reinterpret_cast<const uint4*>(
+                                x + (static_cast<size_t>(img * p.h + ih) * p.w + iw) * C))
+                          : make_uint4(0, 0, 0, 0);
+    }
+  float acc[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t] = KIND == 2 ? -INFINITY : 0.f;
+  int cnt = 0;
+#pragma unroll
+  for (int q = 0; q < K * K; ++q) {
+    if (!ok[q]) continue;
+    ++cnt;
+    float f[8];
+    bf16x8_to_f32(v[q], f);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t] = KIND == 2 ? fmaxf(acc[t], f[t]) : acc[t] + f[t];
+  }
+  if (KIND == 3) {
+    const float inv = 1.f / static_cast<float>(cnt);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t] *= inv;
+  }
+  *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) +
+                            (static_cast<size_t>(row) * p.wo + ow) * C + g * 8) = f32_to_bf16x8(acc);
+}
+
 __global__ void pool_bf16_kernel(PoolParams p) {
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, G = C >> 3;
@@ -687,8 +736,14 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
   const long per = bf16 ? max_c / 8 : max_c;
   const long work = p.kind == 4 ? static_cast<long>(p.n) * per
                                 : static_cast<long>(p.n) * p.ho * p.wo * per;
+  const dim3 rows_grid(static_cast<unsigned>((p.wo * (max_c / 8) + 255) / 256),
+                       static_cast<unsigned>(p.n * p.ho));
   if (bf16 && p.kind == 4)
     gap_bf16_kernel<<<dim3(p.n, (max_c + 63) / 64), 256, 0, s>>>(p);
+  else if (bf16 && p.kind == 2 && p.k == 3)
+    pool_k_bf16_kernel<3, 2><<<rows_grid, 256, 0, s>>>(p);
+  else if (bf16 && p.kind == 3 && p.k == 2)
+    pool_k_bf16_kernel<2, 3><<<rows_grid, 256, 0, s>>>(p);
   else if (bf16)
     pool_bf16_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
   else
