@@ -135,6 +135,14 @@ struct ssn_engine {
   size_t buf_bytes = 0;
   void* d_raw = nullptr;
   size_t raw_img_bytes = 0;
+  // Host inputs are staged through two device buffers on a copy stream, so
+  // the H2D of forward i+1 overlaps the graphs of forward i; a 2-slot ring
+  // guarded by events, then one device copy into d_raw (which the graphs read).
+  void* d_stage[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t stage_ready[2] = {nullptr, nullptr};
+  cudaEvent_t stage_free[2] = {nullptr, nullptr};
+  int stage_slot = 0;
   float* d_logits = nullptr;
   float* d_se = nullptr;  // squeeze-excite scratch: pooled + gate [max_batch][se_cmax]
   int se_cmax = 0;
@@ -700,6 +708,12 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     e->raw_img_bytes = raw_image_bytes(*desc);
     CUDA_TRY(cudaMalloc(&e->d_raw, e->raw_img_bytes * desc->max_batch));
     CUDA_TRY(cudaMemset(e->d_raw, 0, e->raw_img_bytes * desc->max_batch));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaMalloc(&e->d_stage[k], e->raw_img_bytes * desc->max_batch));
+      CUDA_TRY(cudaEventCreateWithFlags(&e->stage_ready[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&e->stage_free[k], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaMalloc(&e->d_logits, static_cast<size_t>(desc->max_batch) * desc->num_classes * 4));
     int se_hmax = 0;
     for (const OpSpec& o : e->net.ops)
@@ -729,6 +743,12 @@ void ssn_destroy(ssn_engine* e) {
   }
   for (int i = 0; i < NBUF; ++i) cudaFree(e->bufs[i]);
   cudaFree(e->d_raw);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(e->d_stage[k]);
+    if (e->stage_ready[k]) cudaEventDestroy(e->stage_ready[k]);
+    if (e->stage_free[k]) cudaEventDestroy(e->stage_free[k]);
+  }
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   cudaFree(e->d_logits);
   cudaFree(e->d_se);
   cudaFree(e->d_rowptr);
@@ -823,7 +843,27 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
       e->dirty = false;
       ++kernels;
     }
-    if (x) CUDA_TRY(cudaMemcpyAsync(e->d_raw, x, e->raw_img_bytes * count, cudaMemcpyDefault, s));
+    if (x) {
+      const size_t bytes = e->raw_img_bytes * count;
+      cudaPointerAttributes attr{};
+      const bool host = cudaPointerGetAttributes(&attr, x) != cudaSuccess ||
+                        attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeUnregistered;
+      cudaGetLastError();  // clear a failed query on an unregistered pointer
+      if (host) {
+        // H2D on the copy stream into a free staging slot (overlaps the
+        // previous forward's graphs), then a device copy on the compute stream
+        const int k = e->stage_slot;
+        e->stage_slot ^= 1;
+        CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->stage_free[k], 0));
+        CUDA_TRY(cudaMemcpyAsync(e->d_stage[k], x, bytes, cudaMemcpyHostToDevice, e->copy_stream));
+        CUDA_TRY(cudaEventRecord(e->stage_ready[k], e->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(s, e->stage_ready[k], 0));
+        CUDA_TRY(cudaMemcpyAsync(e->d_raw, e->d_stage[k], bytes, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(cudaEventRecord(e->stage_free[k], s));
+      } else {
+        CUDA_TRY(cudaMemcpyAsync(e->d_raw, x, bytes, cudaMemcpyDefault, s));
+      }
+    }
     for (size_t si = 0; si < e->net.segments.size(); ++si) {
       if (!sub.seg_run[si]) continue;  // every block skipped: input passes through
       auto it = e->graphs.find(graph_key(static_cast<int>(si), sub.seg_var[si], profiled_batch));
@@ -936,7 +976,7 @@ int ssn_query(ssn_engine* e, ssn_stats* out) {
       out->norm_table_bytes += s.norm_bytes;
       out->max_subnet_stat_bytes = std::max(out->max_subnet_stat_bytes, s.stat_bytes);
     }
-    out->arena_bytes = e->buf_bytes * NBUF + e->raw_img_bytes * e->desc.max_batch;
+    out->arena_bytes = e->buf_bytes * NBUF + 3 * e->raw_img_bytes * e->desc.max_batch;
     out->active_subnet = e->active;
     out->graphs_built = static_cast<uint32_t>(e->graphs.size());
     out->last_forward_kernels = e->last_kernels;
