@@ -50,29 +50,61 @@ __global__ void embed_ln_kernel(EmbedParams p) {
 }
 
 // ---------------------------------------------------------------- LayerNorm
-__global__ void layernorm_kernel(LnParams p) {
+// One warp per row; each lane holds NV 16-byte vectors (8 columns each) of
+// the row in registers: hid = 256 * NV (BERT-base: 768 -> NV = 3).  Loads and
+// stores are 16-byte and coalesced; gamma/beta as float4 pairs.  (The first
+// version read 2-byte scalars into a dynamically indexed local array.)
+template <int NV>
+__global__ void __launch_bounds__(256) layernorm_kernel(LnParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.rows) return;
-  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(warp) * p.hid;
-  float v[32];
-  int cnt = 0;
+  const uint4* x = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) +
+                                                  static_cast<long>(warp) * p.hid);
+  float v[NV][8];
   float sum = 0.f;
-  for (int c = lane; c < p.hid; c += 32, ++cnt) {
-    v[cnt] = bf2f(x[c]);
-    sum += v[cnt];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const uint4 u = __ldg(x + j * 32 + lane);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      v[j][2 * q] = f.x;
+      v[j][2 * q + 1] = f.y;
+      sum += f.x + f.y;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const float mean = sum / p.hid;
   float var = 0.f;
-  for (int i = 0; i < cnt; ++i) var += (v[i] - mean) * (v[i] - mean);
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) var += (v[j][q] - mean) * (v[j][q] - mean);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
   const float inv = rsqrtf(var / p.hid + 1e-12f);
-  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y) + static_cast<long>(warp) * p.hid;
-  cnt = 0;
-  for (int c = lane; c < p.hid; c += 32, ++cnt)
-    y[c] = __float2bfloat16_rn((v[cnt] - mean) * inv * p.gamma[c] + p.beta[c]);
+  uint4* y = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + static_cast<long>(warp) * p.hid);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = (j * 32 + lane) * 8;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.gamma + c + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.beta + c));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.beta + c + 4));
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    float o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = (v[j][q] - mean) * inv * g[q] + bb[q];
+    uint4 u;
+    u.x = pack_bf16x2(o[0], o[1]);
+    u.y = pack_bf16x2(o[2], o[3]);
+    u.z = pack_bf16x2(o[4], o[5]);
+    u.w = pack_bf16x2(o[6], o[7]);
+    y[j * 32 + lane] = u;
+  }
 }
 
 // ---------------------------------------------------------------- token 0
@@ -214,7 +246,14 @@ cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_layernorm(const LnParams& p, cudaStream_t s) {
-  layernorm_kernel<<<static_cast<int>((static_cast<long>(p.rows) * 32 + 255) / 256), 256, 0, s>>>(p);
+  const int grid = static_cast<int>((static_cast<long>(p.rows) * 32 + 255) / 256);
+  switch (p.hid) {
+    case 256: layernorm_kernel<1><<<grid, 256, 0, s>>>(p); break;
+    case 512: layernorm_kernel<2><<<grid, 256, 0, s>>>(p); break;
+    case 768: layernorm_kernel<3><<<grid, 256, 0, s>>>(p); break;
+    case 1024: layernorm_kernel<4><<<grid, 256, 0, s>>>(p); break;
+    default: return cudaErrorInvalidValue;  // hidden width must be 256 * {1..4}
+  }
   return cudaGetLastError();
 }
 
