@@ -68,10 +68,10 @@ constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
 // (SSN_TC_DEBUG=8 isolation) because every tile re-read the same weights.
 constexpr int TC_RB_BYTES = 96 * 1024;
 
-template <int BN_MAX, int STAGES, int KPS, int RESB = 0>
+template <int BN_MAX, int STAGES, int KPS, int RESB = 0, int CG = 1>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr int B_BYTES = BN_MAX * TC_BK * 2;
+  static constexpr int B_BYTES = BN_MAX / CG * TC_BK * 2;  // CG = 2: this CTA's half of N
   static constexpr int RB_BLOCKS = RESB ? TC_RB_BYTES / B_BYTES : 0;
   static constexpr int STAGE_BYTES = KPS * (A_BYTES + (RESB ? 0 : B_BYTES));
   // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
@@ -120,10 +120,17 @@ struct EpiIn {
 // ragged output slice (cout % 8 != 0; BERT head).  One instance per epilogue
 // keeps each compact: an inlined erff/tanhf + scalar tail tripled the SASS of
 // the ReLU kernel and halved its throughput through I-cache misses.
-template <int BN_MAX, int STAGES, int KPS, int EPI, int RESB>
+// CG = 2: a cluster of two CTAs computes one 256 x bn tile with
+// tcgen05.mma.cta_group::2 (issued by CTA 0).  Each CTA loads its own 128
+// A rows and half of B (bn/2 rows) into the same smem offsets, so per SM the
+// operand stream per MMA cycle drops by a third (bn = 256: 32 KB per 512
+// cycles instead of 48 KB) — the per-SM TMA rate (tools/ubench/tma_rate.cu)
+// is what bounds the 1-CTA kernel on the big tensor-bound layers.
+template <int BN_MAX, int STAGES, int KPS, int EPI, int RESB, int CG = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
-  using C = TcCfg<BN_MAX, STAGES, KPS, RESB>;
+  using C = TcCfg<BN_MAX, STAGES, KPS, RESB, CG>;
+  static_assert(CG == 1 || (RESB == 0 && KPS == 1), "2-CTA mode streams both operands");
   constexpr int NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned for SW128; offset arithmetic on smem_raw keeps the shared
@@ -143,10 +150,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
   const int bn = p.bn;
-  const int mt = (p.M + TC_BM - 1) / TC_BM;
+  const int mt = (p.M + TC_BM * CG - 1) / (TC_BM * CG);  // CG = 2: 256-row pair tiles
   const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
   const int tiles = mt * nt;
-  if (static_cast<int>(blockIdx.x) >= tiles) return;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int unit0 = static_cast<int>(blockIdx.x) / CG;     // this CTA's (pair's) first tile
+  const int ustep = static_cast<int>(gridDim.x) / CG;
+  if (unit0 >= tiles) return;  // both CTAs of a pair agree
   // Epilogue work split: wide tiles (>= TC_EPI_GROUPS 32-column chunks) are
   // striped chunk-wise across all groups; narrow ones go whole to one group
   // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
@@ -170,16 +180,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], stripe ? TC_EPI_WARPS : 4);  // warps that drain one tile
+      // warps that drain one tile (CG = 2: both CTAs' epilogues arrive on CTA 0's)
+      mbar_init(&tempty[a], (stripe ? TC_EPI_WARPS : 4) * CG);
     }
     mbar_init(bfull, 1);
     fence_mbar_init();
     tma_prefetch(&wmap);
     tma_prefetch(&dp->amap);
   }
-  if (warp == TC_MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == TC_MMA_WARP) {
+    if (CG == 2)
+      tmem2_alloc(tmem_slot, C::TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();  // the peer's barriers exist before any remote arrival / TMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
@@ -216,9 +233,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     int g = 0;  // stage counter (ring position)
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t / nt) * TC_BM;
-      const int n0 = (t % nt) * bn;
+    for (int t = unit0; t < tiles; t += ustep) {
+      const int m0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM;  // this CTA's rows
+      const int n0 = (t % nt) * bn + static_cast<int>(rank) * (bn / CG);      // this CTA's B rows
       const int img = m0 / hwo;
       const int rem = m0 - img * hwo;
       const int oh = rem / p.wo;
@@ -236,8 +253,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&empty[s], ph ^ 1);
         }
         const int nsub = min(KPS, nk - kb);
-        if (leader) {
-          const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES);
+        if (leader && rank == 0) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
+          const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
           const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
           const uint32_t tx = nsub * (role_b ? b_tx : a_tx);
           if (tx) mbar_arrive_expect_tx(&full[s], tx);
@@ -247,17 +264,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < KPS; ++j) {
           if (j < nsub) {
             if (leader && !role_b) {
+              uint8_t* dst = sA + (s * KPS + j) * C::A_BYTES;
               if (p.dbg & 4) {
               } else if (pointwise) {  // 1x1 stride 1: plain 2-D tile of the [M][cin_a] matrix
-                tma_load_2d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, m0);
+                if (CG == 2) tma2_load_2d(dst, amap, &full[s], cb * TC_BK, m0);
+                else tma_load_2d(dst, amap, &full[s], cb * TC_BK, m0);
+              } else if (CG == 2) {
+                tma2_im2col_4d(dst, amap, &full[s], cb * TC_BK, w0, h0, img,
+                               static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
               } else {
-                tma_im2col_4d(sA + (s * KPS + j) * C::A_BYTES, amap, &full[s], cb * TC_BK, w0, h0,
-                              img, static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
+                tma_im2col_4d(dst, amap, &full[s], cb * TC_BK, w0, h0, img,
+                              static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
               }
             }
-            if (leader && role_b && !(p.dbg & 8))
-              tma_load_3d(sB + (s * KPS + j) * C::B_BYTES, &wmap, &full[s], cb * TC_BK,
-                          (tr + koff) * p.k_max + (ts + koff), n0);
+            if (leader && role_b && !(p.dbg & 8)) {
+              uint8_t* dst = sB + (s * KPS + j) * C::B_BYTES;
+              if (CG == 2)
+                tma2_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+              else
+                tma_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+            }
             if (++cb == cblocks) {
               cb = 0;
               if (++ts == ka) {
@@ -295,7 +321,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       return min(nchunk, (left + 31) / 32);
     };
     auto fetch = [&](EpiIn& in, int t, int c) {
-      const int m0 = (t / nt) * TC_BM + quarter * 32;
+      const int m0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
       const int cc = c * 32;
       const int col = (t % nt) * bn + cc + seg * 8;
       const bool colok = col < d.cout && cc + seg * 8 < bn;
@@ -351,13 +377,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool out_f32 = p.out_f32 != 0;
     // Every tile is drained by all TC_EPI_GROUPS groups: group g takes the
     // 32-column chunks c = g, g + G, ... (more warps in flight per tile than
+    // tempty lives in CTA 0 of a pair (its MMA warp waits on it)
+    auto arrive_tempty = [&](int a) {
+      if (CG == 2)
+        mbar_arrive_cluster(mapa_shared(&tempty[a], 0));
+      else
+        mbar_arrive(&tempty[a]);
+    };
     // alternating whole tiles between two groups, which left the epilogue
     // latency-bound).  A group without a chunk in a tile still waits for the
     // accumulator and arrives on tempty (the barrier counts every warp).
     const int i_step = stripe ? 1 : TC_EPI_GROUPS, c0 = stripe ? group : 0;
     const int c_step = stripe ? TC_EPI_GROUPS : 1;
     int i = stripe ? 0 : group;  // tile ordinal
-    int t = blockIdx.x + i * static_cast<int>(gridDim.x);
+    int t = unit0 + i * ustep;
     int c = c0;
     EpiIn cur;  // this chunk's SubnetNorm row + residual (no register prefetch:
                 // 12 warps hide the latency, and 512 threads cap registers at 128)
@@ -366,7 +399,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (cn >= chunks_of(t)) {
         cn = c0;
         inx = i + i_step;
-        tn = t + i_step * static_cast<int>(gridDim.x);
+        tn = t + i_step * ustep;
       }
       // operands of this chunk, issued before the accumulator wait / TMEM load
       if (!(p.dbg & 1) && c < chunks_of(t)) fetch(cur, t, c);
@@ -384,13 +417,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (c >= chunks_of(t)) {  // no chunk of this tile for this group
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[a]);
+        if (lane == 0) arrive_tempty(a);
         t = tn;
         c = cn;
         i = inx;
         continue;
       }
-      const int m0 = (t / nt) * TC_BM + quarter * 32;
+      const int m0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
       const int cc = c * 32;
       const int col = (t % nt) * bn + cc + seg * 8;
       const bool colok = col < d.cout && cc + seg * 8 < bn;
@@ -412,7 +445,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (inx != i) {  // this warp's last chunk of the tile is out of TMEM: free the accumulator
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[a]);
+        if (lane == 0) arrive_tempty(a);
       }
       const long long tsec = prof ? clock64() : 0;
       if (colok && !(p.dbg & 1)) {
@@ -501,11 +534,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       c = cn;
       i = inx;
     }
-  } else if (warp == TC_MMA_WARP) {
+  } else if (warp == TC_MMA_WARP && rank == 0) {
     // ============================================================ MMA issuer
     // Converged warp, elected lane issues (tc_mma_bf16_elect); descriptors
     // are a base plus 16-byte-unit offsets (SW128: K step = +32 B).
-    const uint32_t idesc = umma_idesc_bf16(bn);
+    const uint32_t idesc = umma_idesc_bf16(bn, TC_BM * CG);
     const uint64_t a_base = umma_desc_sw128(smem_u32(sA));
     const uint64_t b_base = umma_desc_sw128(smem_u32(sB));
     if (RESB) {
@@ -513,7 +546,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
     }
     int g = 0, i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+    for (int t = unit0; t < tiles; t += ustep, ++i) {
       const int a = i % NACC;
       const uint32_t use = static_cast<uint32_t>(i / NACC);
       if (prof) {
@@ -544,15 +577,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint64_t bd =
                 b_base + static_cast<uint64_t>(((RESB ? kb + j : s * KPS + j) * C::B_BYTES) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < TC_BK / 16; ++kk)
-              if (!(p.dbg & 2))
+            for (int kk = 0; kk < TC_BK / 16; ++kk) {
+              if (p.dbg & 2) continue;
+              if (CG == 2)
+                tc2_mma_bf16_elect(acc, ad + static_cast<uint64_t>(kk * 2),
+                                   bd + static_cast<uint64_t>(kk * 2), idesc,
+                                   ((kb + j) | kk) != 0 ? 1u : 0u);
+              else
                 tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(kk * 2),
                                   bd + static_cast<uint64_t>(kk * 2), idesc,
                                   ((kb + j) | kk) != 0 ? 1u : 0u);
+            }
           }
         }
-        tc_commit_elect(&empty[s]);
-        if (kb + KPS >= nk) tc_commit_elect(&tfull[a]);
+        if (CG == 2) {  // free the stage / publish the accumulator in BOTH CTAs
+          tc2_commit_mc_elect(&empty[s]);
+          if (kb + KPS >= nk) tc2_commit_mc_elect(&tfull[a]);
+        } else {
+          tc_commit_elect(&empty[s]);
+          if (kb + KPS >= nk) tc_commit_elect(&tfull[a]);
+        }
         __syncwarp();
       }
     }
@@ -562,9 +606,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
            clock64() - t_begin, w_wait, w_wait2);
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();  // neither CTA leaves while the pair's MMA / arrivals may touch it
   if (warp == TC_MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
+    if (CG == 2)
+      tmem2_dealloc(tmem, C::TMEM_COLS);
+    else
+      tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -679,18 +727,18 @@ int choose_bn(int cout_max, long M) {
 // Instances (BN_MAX, STAGES, K blocks per stage): the operand ring plus the
 // 36 KB epilogue staging fill the 227 KB of shared memory; resident-B
 // instances trade ring stages for the 96 KB weight block.
-#define SSN_TC_INSTANCES(X) X(64, 7, 1, 0) X(128, 5, 1, 0) X(256, 3, 1, 0) \
-  X(64, 4, 1, 1) X(128, 4, 1, 1) X(256, 4, 1, 1)
+#define SSN_TC_INSTANCES(X) X(64, 7, 1, 0, 1) X(128, 5, 1, 0, 1) X(256, 3, 1, 0, 1) \
+  X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2)
 
 cudaError_t init_conv_tc() {
-#define SSN_TC_ATTR(BN, ST, KPS, RB)                                                      \
+#define SSN_TC_ATTR(BN, ST, KPS, RB, CG)                                                  \
   {                                                                                       \
-    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, KPS, 0, RB>,        \
-                                               conv_tc_kernel<BN, ST, KPS, 1, RB>,        \
-                                               conv_tc_kernel<BN, ST, KPS, 2, RB>};       \
+    void (*fns[3])(ConvParams, CUtensorMap) = {conv_tc_kernel<BN, ST, KPS, 0, RB, CG>,    \
+                                               conv_tc_kernel<BN, ST, KPS, 1, RB, CG>,    \
+                                               conv_tc_kernel<BN, ST, KPS, 2, RB, CG>};   \
     for (auto fn : fns) {                                                                 \
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           TcCfg<BN, ST, KPS, RB>::SMEM);                 \
+                                           TcCfg<BN, ST, KPS, RB, CG>::SMEM);             \
       if (e != cudaSuccess) return e;                                                     \
     }                                                                                     \
   }
@@ -699,35 +747,75 @@ cudaError_t init_conv_tc() {
   return cudaSuccess;
 }
 
-template <int BN_MAX, int STAGES, int KPS, int RESB>
+template <int BN_MAX, int STAGES, int KPS, int RESB, int CG = 1>
 static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
-  using C = TcCfg<BN_MAX, STAGES, KPS, RESB>;
-  const long tiles = static_cast<long>((p.M + TC_BM - 1) / TC_BM) * ((p.cout_max + p.bn - 1) / p.bn);
-  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  if (p.act > 2 || (p.cout_max & 7) != 0 || p.ragged)
-    conv_tc_kernel<BN_MAX, STAGES, KPS, 2, RESB><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
-  else if (p.act == 2)
-    conv_tc_kernel<BN_MAX, STAGES, KPS, 1, RESB><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
-  else
-    conv_tc_kernel<BN_MAX, STAGES, KPS, 0, RESB><<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
-  return cudaGetLastError();
+  using C = TcCfg<BN_MAX, STAGES, KPS, RESB, CG>;
+  const long tiles = static_cast<long>((p.M + TC_BM * CG - 1) / (TC_BM * CG)) *
+                     ((p.cout_max + p.bn - 1) / p.bn);
+  void (*fn)(ConvParams, CUtensorMap) =
+      (p.act > 2 || (p.cout_max & 7) != 0 || p.ragged) ? conv_tc_kernel<BN_MAX, STAGES, KPS, 2, RESB, CG>
+      : p.act == 2                                      ? conv_tc_kernel<BN_MAX, STAGES, KPS, 1, RESB, CG>
+                                                        : conv_tc_kernel<BN_MAX, STAGES, KPS, 0, RESB, CG>;
+  if (CG == 1) {
+    const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+    fn<<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
+    return cudaGetLastError();
+  }
+  // clusters of 2 CTAs (one per pair tile), at most one pair per 2 SMs
+  const long pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(pairs * 2));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, p, wmap);
 }
 
-cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s) {
+static int tc_debug() {
   static const int dbg = [] {
     const char* e = getenv("SSN_TC_DEBUG");
     return e ? atoi(e) : 0;
   }();
+  return dbg;
+}
+
+static bool resident_b(const ConvParams& p) {
+  const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
+  return !(tc_debug() & 512) && p.cout_max <= p.bn && nk_max * p.bn * TC_BK * 2 <= TC_RB_BYTES;
+}
+
+// Pair tiles (cta_group::2) for bn > 128 streamed-B convs; the caller encodes
+// the weight map with bn / 2 rows per box when this returns true.
+// Measured (tools/mb_ncu.sh): pairs win on long-K layers (3x3 720 @ 7 px
+// -20%, 1x1 2048->720 -6%) and lose on short-K ones where the per-tile
+// epilogue dominates (1x1 256->256 +15%), so they need >= 16 K blocks.
+bool conv_tc_use_pairs(const ConvParams& p) {
+  const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
+  return p.bn > 128 && nk_max >= 16 && !resident_b(p) && !(tc_debug() & 16384) && p.act <= 2 &&
+         (p.cout_max & 7) == 0 && !p.ragged && !p.out_f32;
+}
+
+cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s) {
+  const int dbg = tc_debug();
   ConvParams p = p_in;
   p.dbg = dbg;
   // Resident B: the max-shape slice is one N tile (so is every subnet's) and
   // all its K blocks fit TC_RB_BYTES.
-  const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
-  const bool resb = !(p.dbg & 512) && p.cout_max <= p.bn && nk_max * p.bn * TC_BK * 2 <= TC_RB_BYTES;
+  const bool resb = resident_b(p);
   if (p.bn <= 64) return resb ? launch_impl<64, 4, 1, 1>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
   if (p.bn <= 128)
     return resb ? launch_impl<128, 4, 1, 1>(p, wmap, s) : launch_impl<128, 5, 1, 0>(p, wmap, s);
-  return resb ? launch_impl<256, 4, 1, 1>(p, wmap, s) : launch_impl<256, 3, 1, 0>(p, wmap, s);
+  if (resb) return launch_impl<256, 4, 1, 1>(p, wmap, s);
+  // bn > 128: pair tiles (cta_group::2) unless SSN_TC_DEBUG & 16384
+  if (p.cg2) return launch_impl<256, 5, 1, 0, 2>(p, wmap, s);
+  return launch_impl<256, 3, 1, 0>(p, wmap, s);
 }
 
 }  // namespace ssn

@@ -34,6 +34,7 @@ int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, in
 int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
                  int pad);
 int choose_bn(int cout_max, long M);
+bool conv_tc_use_pairs(const ConvParams& p);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t init_conv_halo();
@@ -317,8 +318,10 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
         CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
       } else if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M);
+        p.cg2 = conv_tc_use_pairs(p);
         CUtensorMap wmap{};
-        if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn) != 0)
+        if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout,
+                            p.cg2 ? p.bn / 2 : p.bn) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
         CUDA_TRY(launch_conv_tc(p, wmap, s));
       } else if (bf) {
@@ -1070,8 +1073,9 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.bn = choose_bn(cout_max, p.M);
     // ragged slice, or SubnetNorm vectors the vector epilogue cannot load
     p.ragged = (cout & 7) != 0 || ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) != 0;
+    p.cg2 = conv_tc_use_pairs(p);
     CUtensorMap wmap{};
-    if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn) != 0)
+    if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.cg2 ? p.bn / 2 : p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
     CUDA_TRY(launch_conv_tc(p, wmap, s));
   });
