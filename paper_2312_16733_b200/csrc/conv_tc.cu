@@ -728,7 +728,7 @@ int choose_bn(int cout_max, long M) {
 // 36 KB epilogue staging fill the 227 KB of shared memory; resident-B
 // instances trade ring stages for the 96 KB weight block.
 #define SSN_TC_INSTANCES(X) X(64, 7, 1, 0, 1) X(128, 5, 1, 0, 1) X(256, 3, 1, 0, 1) \
-  X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2)
+  X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2) X(128, 7, 1, 0, 2)
 
 cudaError_t init_conv_tc() {
 #define SSN_TC_ATTR(BN, ST, KPS, RB, CG)                                                  \
@@ -798,7 +798,7 @@ static bool resident_b(const ConvParams& p) {
 // epilogue dominates (1x1 256->256 +15%), so they need >= 16 K blocks.
 bool conv_tc_use_pairs(const ConvParams& p) {
   const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
-  return p.bn > 128 && nk_max >= 16 && !resident_b(p) && !(tc_debug() & 16384) && p.act <= 2 &&
+  return p.bn >= 128 && nk_max >= 16 && !resident_b(p) && !(tc_debug() & 16384) && p.act <= 2 &&
          (p.cout_max & 7) == 0 && !p.ragged && !p.out_f32;
 }
 
@@ -810,8 +810,11 @@ cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cuda
   // all its K blocks fit TC_RB_BYTES.
   const bool resb = resident_b(p);
   if (p.bn <= 64) return resb ? launch_impl<64, 4, 1, 1>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
-  if (p.bn <= 128)
-    return resb ? launch_impl<128, 4, 1, 1>(p, wmap, s) : launch_impl<128, 5, 1, 0>(p, wmap, s);
+  if (p.bn <= 128) {
+    if (resb) return launch_impl<128, 4, 1, 1>(p, wmap, s);
+    if (p.cg2) return launch_impl<128, 7, 1, 0, 2>(p, wmap, s);  // bn == 128 pair tiles
+    return launch_impl<128, 5, 1, 0>(p, wmap, s);
+  }
   if (resb) return launch_impl<256, 4, 1, 1>(p, wmap, s);
   // bn > 128: pair tiles (cta_group::2) unless SSN_TC_DEBUG & 16384
   if (p.cg2) return launch_impl<256, 5, 1, 0, 2>(p, wmap, s);
