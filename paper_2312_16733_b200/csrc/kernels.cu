@@ -623,63 +623,85 @@ __global__ void se_pool_kernel(SEParams p) {
 // rows are read once per SE_NB samples and every SM has work.  hid lives in
 // the tail of the gate scratch (fp32 [n][se_max]).
 constexpr int SE_NB = 8;
-constexpr int SE_ROWS = 32;  // output rows per block (8 warps x 4)
 
 __device__ __forceinline__ float* se_hid(const SEParams& p) {
   return p.gate + static_cast<long>(p.n) * p.c_max;
 }
 
-__global__ void se_reduce_kernel(SEParams p) {
+// One warp per output row; each lane reads 8 weights (16 B) and the 8
+// matching pooled values of every sample per step, so a 1152-wide row is 4.5
+// fully independent steps (the scalar version walked C / 32 dependent
+// 2-byte steps per row and was latency-bound at ~65 us per launch).
+__device__ __forceinline__ void ld_f32x8(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+__global__ void __launch_bounds__(256) se_reduce_kernel(SEParams p) {
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
   const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.w_reduce);
+  const int j = blockIdx.y * 8 + warp;  // output row
+  if (j >= mid) return;
+  const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.w_reduce) + static_cast<long>(j) * p.w_ld;
   float* hid = se_hid(p);
-  for (int j = blockIdx.y * SE_ROWS + warp; j < min(mid, (blockIdx.y + 1) * SE_ROWS); j += 8) {
-    float acc[SE_NB];
+  float acc[SE_NB];
 #pragma unroll
-    for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
-    for (int c = lane; c < C; c += 32) {
-      const float wv = __bfloat162float(wr[static_cast<long>(j) * p.w_ld + c]);
-#pragma unroll
-      for (int b = 0; b < SE_NB; ++b)
-        if (b < nb) acc[b] += wv * p.pooled[static_cast<long>(n0 + b) * p.c_max + c];
-    }
+  for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
+  for (int c = lane * 8; c < C; c += 256) {
+    float w[8];
+    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wr + c)), w);
 #pragma unroll
     for (int b = 0; b < SE_NB; ++b) {
+      if (b >= nb) break;
+      float x[8];
+      ld_f32x8(p.pooled + static_cast<long>(n0 + b) * p.c_max + c, x);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-      if (lane == 0 && b < nb) hid[static_cast<long>(n0 + b) * p.se_max + j] = fmaxf(acc[b] + p.b_reduce[j], 0.f);
+      for (int q = 0; q < 8; ++q) acc[b] += w[q] * x[q];
     }
+  }
+#pragma unroll
+  for (int b = 0; b < SE_NB; ++b) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+    if (lane == 0 && b < nb) hid[static_cast<long>(n0 + b) * p.se_max + j] = fmaxf(acc[b] + p.b_reduce[j], 0.f);
   }
 }
 
-__global__ void se_expand_kernel(SEParams p) {
+__global__ void __launch_bounds__(256) se_expand_kernel(SEParams p) {
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
   const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const __nv_bfloat16* we = static_cast<const __nv_bfloat16*>(p.w_expand);
+  const int c = blockIdx.y * 8 + warp;  // output channel
+  if (c >= C) return;
+  const __nv_bfloat16* we = static_cast<const __nv_bfloat16*>(p.w_expand) + static_cast<long>(c) * p.se_max;
   const float* hid = se_hid(p);
-  for (int c = blockIdx.y * SE_ROWS + warp; c < min(C, (blockIdx.y + 1) * SE_ROWS); c += 8) {
-    float acc[SE_NB];
+  float acc[SE_NB];
 #pragma unroll
-    for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
-    for (int j = lane; j < mid; j += 32) {
-      const float wv = __bfloat162float(we[static_cast<long>(c) * p.se_max + j]);
-#pragma unroll
-      for (int b = 0; b < SE_NB; ++b)
-        if (b < nb) acc[b] += wv * hid[static_cast<long>(n0 + b) * p.se_max + j];
-    }
+  for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
+  for (int j = lane * 8; j < mid; j += 256) {
+    float w[8];
+    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(we + j)), w);
 #pragma unroll
     for (int b = 0; b < SE_NB; ++b) {
+      if (b >= nb) break;
+      float x[8];
+      ld_f32x8(hid + static_cast<long>(n0 + b) * p.se_max + j, x);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-      if (lane == 0 && b < nb)
-        p.gate[static_cast<long>(n0 + b) * p.c_max + c] =
-            fminf(fmaxf(acc[b] + p.b_expand[c] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+      for (int q = 0; q < 8; ++q) acc[b] += w[q] * x[q];
     }
+  }
+#pragma unroll
+  for (int b = 0; b < SE_NB; ++b) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+    if (lane == 0 && b < nb)
+      p.gate[static_cast<long>(n0 + b) * p.c_max + c] =
+          fminf(fmaxf(acc[b] + p.b_expand[c] + 3.f, 0.f), 6.f) * (1.f / 6.f);
   }
 }
 
@@ -776,8 +798,8 @@ cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
 cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
   se_pool_kernel<<<dim3(p.n, (p.c_max + 63) / 64), 256, 0, s>>>(p);
   const int nbk = (p.n + SE_NB - 1) / SE_NB;
-  se_reduce_kernel<<<dim3(nbk, (p.se_max + SE_ROWS - 1) / SE_ROWS), 256, 0, s>>>(p);
-  se_expand_kernel<<<dim3(nbk, (p.c_max + SE_ROWS - 1) / SE_ROWS), 256, 0, s>>>(p);
+  se_reduce_kernel<<<dim3(nbk, (p.se_max + 7) / 8), 256, 0, s>>>(p);   // one warp per row
+  se_expand_kernel<<<dim3(nbk, (p.c_max + 7) / 8), 256, 0, s>>>(p);
   se_scale_kernel<<<grid_for(static_cast<long>(p.n) * p.hw * (p.c_max / 8), 256), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
