@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // PDL: upstream activations are read only after this
+  pdl_trigger();
   // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
   const bool prof = (p.dbg & 32) && blockIdx.x == 0;
   long long w_wait = 0, w_wait2 = 0;
@@ -440,8 +442,7 @@ cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int t
   const HaloGeom g = halo_geom(p.w_, p.k_max);
   const long tiles = static_cast<long>(p.n) * ((p.h + g.rt - 1) / g.rt);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
-  conv_halo_kernel<<<grid, HL_THREADS, smem, s>>>(p, wmap);
-  return cudaGetLastError();
+  return launch_pdl(conv_halo_kernel, dim3(grid), dim3(HL_THREADS), smem, s, 1, p, wmap);
 }
 
 }  // namespace ssn

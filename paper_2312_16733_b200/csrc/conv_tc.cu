@@ -199,6 +199,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (CG == 2) cluster_sync();  // the peer's barriers exist before any remote arrival / TMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: everything above touched only smem / TMEM / static descriptors; the
+  // predecessor's activations are read only after this
+  pdl_wait();
+  pdl_trigger();
   // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
   const bool prof = (p.dbg & 32) && blockIdx.x == 0;
   long long w_wait = 0, w_wait2 = 0;
@@ -758,24 +762,12 @@ static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cud
                                                         : conv_tc_kernel<BN_MAX, STAGES, KPS, 0, RESB, CG>;
   if (CG == 1) {
     const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-    fn<<<grid, TC_THREADS, C::SMEM, s>>>(p, wmap);
-    return cudaGetLastError();
+    return launch_pdl(fn, dim3(grid), dim3(TC_THREADS), C::SMEM, s, 1, p, wmap);
   }
   // clusters of 2 CTAs (one per pair tile), at most one pair per 2 SMs
   const long pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(pairs * 2));
-  cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, p, wmap);
+  return launch_pdl(fn, dim3(static_cast<unsigned>(pairs * 2)), dim3(TC_THREADS), C::SMEM, s, 2, p,
+                    wmap);
 }
 
 static int tc_debug() {

@@ -56,6 +56,8 @@ __global__ void input_kernel(InputParams p) {
 // and leave as four 16-byte stores.
 template <bool U8>
 __global__ void __launch_bounds__(256) input_im2col3_kernel(InputParams p) {
+  pdl_wait();
+  pdl_trigger();
   const long npix = static_cast<long>(p.n) * p.ho * p.wo;
   const int st = p.im2col_stride;
   const long hw = static_cast<long>(p.h) * p.w;
@@ -175,6 +177,8 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 // so the hw loads of a channel group are in flight together (one thread per
 // channel group summing hw pixels serially was latency-bound).
 __global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin;
   const int n = blockIdx.x, c0 = blockIdx.y * 64;
@@ -210,6 +214,8 @@ __global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
 // window loop serialised them), 32-bit index math.
 template <int K, int KIND>
 __global__ void __launch_bounds__(256) pool_k_bf16_kernel(PoolParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, G = C >> 3;
   const int row = blockIdx.y;
@@ -741,10 +747,9 @@ cudaError_t launch_input(const InputParams& p, cudaStream_t s) {
   const long npix = static_cast<long>(p.n) * p.ho * p.wo;
   if (p.im2col_k == 3 && p.cpad == 32) {
     const int grid = static_cast<int>(std::min<long>((npix + 255) / 256, 148L * 8));
-    if (p.format == SSN_INPUT_U8_NHWC)
-      input_im2col3_kernel<true><<<grid, 256, 0, s>>>(p);
-    else
-      input_im2col3_kernel<false><<<grid, 256, 0, s>>>(p);
+    return launch_pdl(p.format == SSN_INPUT_U8_NHWC ? input_im2col3_kernel<true>
+                                                   : input_im2col3_kernel<false>,
+                      dim3(grid), dim3(256), 0, s, 1, p);
   } else if (p.im2col_k > 0) {
     input_im2col_kernel<<<grid_for(npix, 128), 128, 0, s>>>(p);
   }
@@ -761,11 +766,11 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
   const dim3 rows_grid(static_cast<unsigned>((p.wo * (max_c / 8) + 255) / 256),
                        static_cast<unsigned>(p.n * p.ho));
   if (bf16 && p.kind == 4)
-    gap_bf16_kernel<<<dim3(p.n, (max_c + 63) / 64), 256, 0, s>>>(p);
+    return launch_pdl(gap_bf16_kernel, dim3(p.n, (max_c + 63) / 64), dim3(256), 0, s, 1, p);
   else if (bf16 && p.kind == 2 && p.k == 3)
-    pool_k_bf16_kernel<3, 2><<<rows_grid, 256, 0, s>>>(p);
+    return launch_pdl(pool_k_bf16_kernel<3, 2>, rows_grid, dim3(256), 0, s, 1, p);
   else if (bf16 && p.kind == 3 && p.k == 2)
-    pool_k_bf16_kernel<2, 3><<<rows_grid, 256, 0, s>>>(p);
+    return launch_pdl(pool_k_bf16_kernel<2, 3>, rows_grid, dim3(256), 0, s, 1, p);
   else if (bf16)
     pool_bf16_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
   else
