@@ -17,6 +17,8 @@ namespace ssn {
 // input staging: host-format images -> NHWC (bf16 padded to 8 ch, or fp32 3 ch)
 
 __global__ void input_kernel(InputParams p) {
+  pdl_wait();
+  pdl_trigger();
   const long npix = static_cast<long>(p.n) * p.h * p.w;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < npix;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -105,6 +107,8 @@ __global__ void __launch_bounds__(256) input_im2col3_kernel(InputParams p) {
 }
 
 __global__ void input_im2col_kernel(InputParams p) {
+  pdl_wait();
+  pdl_trigger();
   const long npix = static_cast<long>(p.n) * p.ho * p.wo;
   const int k = p.im2col_k, st = p.im2col_stride, pad = k / 2;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < npix;
@@ -260,6 +264,8 @@ __global__ void __launch_bounds__(256) pool_k_bf16_kernel(PoolParams p) {
 }
 
 __global__ void pool_bf16_kernel(PoolParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, G = C >> 3;
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
@@ -322,6 +328,8 @@ __global__ void pool_bf16_kernel(PoolParams p) {
 }
 
 __global__ void pool_f32_kernel(PoolParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin;
   const float* x = static_cast<const float*>(p.x);
@@ -370,6 +378,8 @@ __global__ void pool_f32_kernel(PoolParams p) {
 // [c_max][k_max][k_max]; centre crop to the active k.
 
 __global__ void conv_f32_kernel(ConvParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, p.fixed, p.op);
   const long total = static_cast<long>(p.M) * d.cout;
   const float* x = static_cast<const float*>(p.x);
@@ -484,6 +494,8 @@ __device__ __forceinline__ void st_f32x8(uint8_t* dst, const uint4& v) {
 
 template <int S>
 __global__ void __launch_bounds__(256) dw_bf16_kernel(ConvParams p) {
+  pdl_wait();
+  pdl_trigger();
   using T = DwTile<S>;
   extern __shared__ __align__(16) uint8_t dsm[];
   uint8_t* tile = dsm;                 // [IH][IW][32] fp32
@@ -597,6 +609,8 @@ __global__ void __launch_bounds__(256) dw_bf16_kernel(ConvParams p) {
 // pooled[n][c] = mean over hw; grid (n, ceil(C/64)), 256 threads:
 // 8 channel groups x 32 pixel lanes, shared-memory reduction over lanes.
 __global__ void se_pool_kernel(SEParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin;
   const int n = blockIdx.x, c0 = blockIdx.y * 64;
@@ -646,6 +660,8 @@ __device__ __forceinline__ void ld_f32x8(const float* p, float (&f)[8]) {
 }
 
 __global__ void __launch_bounds__(256) se_reduce_kernel(SEParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
   const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
@@ -678,6 +694,8 @@ __global__ void __launch_bounds__(256) se_reduce_kernel(SEParams p) {
 }
 
 __global__ void __launch_bounds__(256) se_expand_kernel(SEParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
   const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
@@ -712,6 +730,8 @@ __global__ void __launch_bounds__(256) se_expand_kernel(SEParams p) {
 }
 
 __global__ void se_scale_kernel(SEParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, G = C >> 3;
   __nv_bfloat16* x = static_cast<__nv_bfloat16*>(p.x);
@@ -750,12 +770,11 @@ cudaError_t launch_input(const InputParams& p, cudaStream_t s) {
     return launch_pdl(p.format == SSN_INPUT_U8_NHWC ? input_im2col3_kernel<true>
                                                    : input_im2col3_kernel<false>,
                       dim3(grid), dim3(256), 0, s, 1, p);
-  } else if (p.im2col_k > 0) {
-    input_im2col_kernel<<<grid_for(npix, 128), 128, 0, s>>>(p);
   }
-  else
-    input_kernel<<<grid_for(static_cast<long>(p.n) * p.h * p.w, 256), 256, 0, s>>>(p);
-  return cudaGetLastError();
+  if (p.im2col_k > 0)
+    return launch_pdl(input_im2col_kernel, dim3(grid_for(npix, 128)), dim3(128), 0, s, 1, p);
+  return launch_pdl(input_kernel, dim3(grid_for(static_cast<long>(p.n) * p.h * p.w, 256)),
+                    dim3(256), 0, s, 1, p);
 }
 
 // `max_c` bounds the grid for the largest subnet; surplus threads exit.
@@ -767,20 +786,17 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
                        static_cast<unsigned>(p.n * p.ho));
   if (bf16 && p.kind == 4)
     return launch_pdl(gap_bf16_kernel, dim3(p.n, (max_c + 63) / 64), dim3(256), 0, s, 1, p);
-  else if (bf16 && p.kind == 2 && p.k == 3)
+  if (bf16 && p.kind == 2 && p.k == 3)
     return launch_pdl(pool_k_bf16_kernel<3, 2>, rows_grid, dim3(256), 0, s, 1, p);
-  else if (bf16 && p.kind == 3 && p.k == 2)
+  if (bf16 && p.kind == 3 && p.k == 2)
     return launch_pdl(pool_k_bf16_kernel<2, 3>, rows_grid, dim3(256), 0, s, 1, p);
-  else if (bf16)
-    pool_bf16_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
-  else
-    pool_f32_kernel<<<grid_for(work, 256), 256, 0, s>>>(p);
-  return cudaGetLastError();
+  if (bf16) return launch_pdl(pool_bf16_kernel, dim3(grid_for(work, 256)), dim3(256), 0, s, 1, p);
+  return launch_pdl(pool_f32_kernel, dim3(grid_for(work, 256)), dim3(256), 0, s, 1, p);
 }
 
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s) {
-  conv_f32_kernel<<<grid_for(static_cast<long>(p.M) * p.cout_max, 128), 128, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(conv_f32_kernel, dim3(grid_for(static_cast<long>(p.M) * p.cout_max, 128)),
+                    dim3(128), 0, s, 1, p);
 }
 
 template <int S>
@@ -791,8 +807,8 @@ static cudaError_t launch_dw_tiles(const ConvParams& p, cudaStream_t s) {
   if (attr != cudaSuccess) return attr;
   const long tiles = static_cast<long>(p.n) * ((p.ho + T::TH - 1) / T::TH) *
                      ((p.wo + T::TW - 1) / T::TW) * ((p.cout_max + DWT_CC - 1) / DWT_CC);
-  dw_bf16_kernel<S><<<static_cast<unsigned>(tiles), 256, T::SMEM, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(dw_bf16_kernel<S>, dim3(static_cast<unsigned>(tiles)), dim3(256), T::SMEM, s,
+                    1, p);
 }
 
 cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
@@ -801,12 +817,17 @@ cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
-  se_pool_kernel<<<dim3(p.n, (p.c_max + 63) / 64), 256, 0, s>>>(p);
+  cudaError_t e = launch_pdl(se_pool_kernel, dim3(p.n, (p.c_max + 63) / 64), dim3(256), 0, s, 1, p);
+  if (e != cudaSuccess) return e;
   const int nbk = (p.n + SE_NB - 1) / SE_NB;
-  se_reduce_kernel<<<dim3(nbk, (p.se_max + 7) / 8), 256, 0, s>>>(p);   // one warp per row
-  se_expand_kernel<<<dim3(nbk, (p.c_max + 7) / 8), 256, 0, s>>>(p);
-  se_scale_kernel<<<grid_for(static_cast<long>(p.n) * p.hw * (p.c_max / 8), 256), 256, 0, s>>>(p);
-  return cudaGetLastError();
+  // one warp per output row
+  e = launch_pdl(se_reduce_kernel, dim3(nbk, (p.se_max + 7) / 8), dim3(256), 0, s, 1, p);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(se_expand_kernel, dim3(nbk, (p.c_max + 7) / 8), dim3(256), 0, s, 1, p);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(se_scale_kernel,
+                    dim3(grid_for(static_cast<long>(p.n) * p.hw * (p.c_max / 8), 256)), dim3(256),
+                    0, s, 1, p);
 }
 
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s) {

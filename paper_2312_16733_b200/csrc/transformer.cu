@@ -19,6 +19,8 @@ __device__ __forceinline__ float bf2f(const __nv_bfloat16 v) { return __bfloat16
 // ---------------------------------------------------------------- embedding + LN
 // one warp per token: x = tok[id] + pos[p] + typ[0]; LayerNorm over hid
 __global__ void embed_ln_kernel(EmbedParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int rows = p.n * p.s;
   if (warp >= rows) return;
@@ -56,6 +58,8 @@ __global__ void embed_ln_kernel(EmbedParams p) {
 // version read 2-byte scalars into a dynamically indexed local array.)
 template <int NV>
 __global__ void __launch_bounds__(256) layernorm_kernel(LnParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.rows) return;
   const uint4* x = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) +
@@ -109,6 +113,8 @@ __global__ void __launch_bounds__(256) layernorm_kernel(LnParams p) {
 
 // ---------------------------------------------------------------- token 0
 __global__ void token0_kernel(Token0Params p) {
+  pdl_wait();
+  pdl_trigger();
   const long total = static_cast<long>(p.n) * (p.c / 8);
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -134,6 +140,8 @@ constexpr int ATT_KLD = ATT_D + 8;   // K row stride (bf16), conflict-free fragm
 constexpr int ATT_VLD = ATT_S + 8;   // V^T row stride
 
 __global__ void __launch_bounds__(256) attention_kernel(AttnParams p) {
+  pdl_wait();
+  pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int heads = d.cin / ATT_D;
   if (static_cast<int>(blockIdx.x) >= p.n * heads) return;  // head beyond the active width
@@ -241,32 +249,29 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnParams p) {
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
   const long warps = static_cast<long>(p.n) * p.s;
-  embed_ln_kernel<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(embed_ln_kernel, dim3(static_cast<int>((warps * 32 + 255) / 256)), dim3(256),
+                    0, s, 1, p);
 }
 
 cudaError_t launch_layernorm(const LnParams& p, cudaStream_t s) {
   const int grid = static_cast<int>((static_cast<long>(p.rows) * 32 + 255) / 256);
   switch (p.hid) {
-    case 256: layernorm_kernel<1><<<grid, 256, 0, s>>>(p); break;
-    case 512: layernorm_kernel<2><<<grid, 256, 0, s>>>(p); break;
-    case 768: layernorm_kernel<3><<<grid, 256, 0, s>>>(p); break;
-    case 1024: layernorm_kernel<4><<<grid, 256, 0, s>>>(p); break;
+    case 256: return launch_pdl(layernorm_kernel<1>, dim3(grid), dim3(256), 0, s, 1, p);
+    case 512: return launch_pdl(layernorm_kernel<2>, dim3(grid), dim3(256), 0, s, 1, p);
+    case 768: return launch_pdl(layernorm_kernel<3>, dim3(grid), dim3(256), 0, s, 1, p);
+    case 1024: return launch_pdl(layernorm_kernel<4>, dim3(grid), dim3(256), 0, s, 1, p);
     default: return cudaErrorInvalidValue;  // hidden width must be 256 * {1..4}
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_token0(const Token0Params& p, cudaStream_t s) {
-  token0_kernel<<<(p.n * (p.c / 8) + 255) / 256, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(token0_kernel, dim3((p.n * (p.c / 8) + 255) / 256), dim3(256), 0, s, 1, p);
 }
 
 // grid = n x max heads; CTAs past the active head count exit
 cudaError_t launch_attention(const AttnParams& p, int max_heads, cudaStream_t s) {
   if (p.s != ATT_S) return cudaErrorInvalidValue;
-  attention_kernel<<<p.n * max_heads, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(attention_kernel, dim3(p.n * max_heads), dim3(256), 0, s, 1, p);
 }
 
 }  // namespace ssn
