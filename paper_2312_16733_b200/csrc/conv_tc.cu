@@ -45,16 +45,18 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
 constexpr int TC_EPI_WARPS = 12;  // 3 groups x 4 TMEM lane quarters
 constexpr int TC_EPI_GROUPS = TC_EPI_WARPS / 4;
-// Warp roles.  Warpgroup 0 = warp 0 A producer, warp 1 MMA issuer, warp 2 B
-// producer (warp 3 idle); warpgroups 1-3 = the 12 epilogue warps.  One
-// thread sustains only ~1 TMA box per ~360 cycles (wait + expect_tx + issue;
-// tools/ubench/tma_rate.cu: 45 B/cycle with 16 KB boxes from one thread, 76
-// with two), less than a K block of N=128 MMAs, so A and B have separate
-// issuers.  512 threads cap registers at 128: the epilogue keeps no
-// register prefetch of the next chunk.
+// Warp roles.  Warpgroup 0 = warps 0, 2, 3 TMA producers, warp 1 MMA issuer;
+// warpgroups 1-3 = the 12 epilogue warps.  One thread sustains only ~1 TMA
+// box per ~360 cycles (wait + expect_tx + issue; tools/ubench/tma_rate.cu:
+// 45 B/cycle with 16 KB boxes from one thread, 76 with two), less than a K
+// block of N=128 MMAs, so the three producers take K blocks round-robin and
+// each loads both operands of its blocks.  512 threads cap registers at
+// 128: the epilogue keeps no register prefetch of the next chunk.
 constexpr int TC_PROD_WARP = 0;
 constexpr int TC_MMA_WARP = 1;
 constexpr int TC_PROD2_WARP = 2;
+constexpr int TC_PROD3_WARP = 3;
+constexpr int TC_NPROD = 3;
 constexpr int TC_EPI_WARP0 = 4;
 constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 512
 
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], RESB ? 1 : 2);  // the A (and B) producers' expect_tx arrivals
+      mbar_init(&full[s], 1);  // the owning producer's expect_tx arrival
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
@@ -208,15 +210,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   long long w_wait = 0, w_wait2 = 0;
   const long long t_begin = prof ? clock64() : 0;
 
-  if (warp == TC_PROD_WARP || (warp == TC_PROD2_WARP && !RESB)) {
+  if (warp == TC_PROD_WARP || warp == TC_PROD2_WARP || warp == TC_PROD3_WARP) {
     // ============================================================ producers
-    // warp 0: A (activations) + the resident-B preload; warp 14: B (weights)
-    const bool role_b = warp == TC_PROD2_WARP;
+    // K block g (ring position) belongs to producer g % TC_NPROD, which loads
+    // its A (activations) and B (weights) boxes; warp 0 also preloads the
+    // resident B.  Safe against mbarrier phase aliasing: a producer reaching
+    // g has filled g - TC_NPROD, which needed g - TC_NPROD - STAGES released,
+    // so g - 2 * STAGES was released too (TC_NPROD <= STAGES).
+    static_assert(TC_NPROD <= STAGES, "producer round-robin needs TC_NPROD <= STAGES");
+    const int pidx = warp == TC_PROD_WARP ? 0 : warp - 1;
     const bool leader = elect_one();
     const CUtensorMap* amap = &dp->amap;
     const int hwo = p.ho * p.wo;
     const bool pointwise = p.k_max == 1 && p.stride == 1;  // A map is 2-D tiled (make_act_map)
-    if (RESB && leader && !role_b) {
+    if (RESB && leader && pidx == 0) {
       // the whole (single-N-tile) weight slice, once per CTA: block kb = (tap, channel block)
       if (p.dbg & 8) {
         mbar_arrive(bfull);
@@ -247,6 +254,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int w0 = ow * p.stride - pad, h0 = oh * p.stride - pad;
       int tr = 0, ts = 0, cb = 0;
       for (int kb = 0; kb < nk; kb += KPS, ++g) {
+        if (g % TC_NPROD != pidx) {  // another producer's block: advance the (tap, channel) walk
+#pragma unroll
+          for (int j = 0; j < KPS; ++j) {
+            if (++cb == cblocks) {
+              cb = 0;
+              if (++ts == ka) {
+                ts = 0;
+                ++tr;
+              }
+            }
+          }
+          continue;
+        }
         const int s = g % STAGES;
         const uint32_t ph = (g / STAGES) & 1;
         if (prof) {
@@ -260,14 +280,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (leader && rank == 0) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
           const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
-          const uint32_t tx = nsub * (role_b ? b_tx : a_tx);
+          const uint32_t tx = nsub * (a_tx + (RESB ? 0u : b_tx));
           if (tx) mbar_arrive_expect_tx(&full[s], tx);
           else mbar_arrive(&full[s]);
         }
 #pragma unroll
         for (int j = 0; j < KPS; ++j) {
           if (j < nsub) {
-            if (leader && !role_b) {
+            if (leader) {
               uint8_t* dst = sA + (s * KPS + j) * C::A_BYTES;
               if (p.dbg & 4) {
               } else if (pointwise) {  // 1x1 stride 1: plain 2-D tile of the [M][cin_a] matrix
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                               static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
               }
             }
-            if (leader && role_b && !(p.dbg & 8)) {
+            if (leader && !RESB && !(p.dbg & 8)) {
               uint8_t* dst = sB + (s * KPS + j) * C::B_BYTES;
               if (CG == 2)
                 tma2_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);

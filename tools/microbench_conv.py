@@ -28,6 +28,20 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (1, 56, 56, 88, 88, 88, 88, 3, 1, 0),
     (64, 56, 56, 88, 88, 256, 256, 1, 1, 0),   # case3 without the residual
     (64, 56, 56, 256, 256, 256, 256, 1, 1, 0), # wide in, wide out
+    (256, 14, 14, 2048, 2048, 2048, 2048, 1, 1, 0),  # compute-bound GEMM probe
+    (256, 14, 14, 512, 512, 512, 512, 3, 1, 0),      # compute-bound 3x3 probe
+    (64, 7, 7, 2048, 2048, 720, 720, 1, 1, 0),       # = case7 (small M)
+    (64, 14, 14, 136, 360, 136, 360, 3, 1, 0),       # min-subnet 14px 3x3
+    (64, 14, 14, 136, 384, 136, 384, 3, 1, 0),       # 20: aligned weights, misaligned act
+    (64, 14, 14, 192, 384, 192, 384, 3, 1, 0),       # 21: aligned both
+    (64, 14, 14, 192, 360, 192, 360, 3, 1, 0),       # 22: aligned act, misaligned weights
+    (64, 14, 14, 384, 384, 384, 384, 3, 1, 0),       # 23: case2 but aligned
+    (64, 7, 7, 2048, 2048, 768, 768, 1, 1, 0),       # 24: case7, N aligned to 256
+    (256, 14, 14, 512, 512, 384, 384, 3, 1, 0),      # 25: bn128 pair tiles, long grid
+    (256, 14, 14, 360, 360, 360, 360, 3, 1, 0),      # 26: case2 at n=256
+    (16, 14, 14, 360, 360, 360, 360, 3, 1, 0),       # 27: case2 at n=16
+    (256, 14, 14, 2048, 2048, 384, 384, 1, 1, 0),    # 28: bn128 pairs, tiled A (vs 25: im2col A)
+    (256, 14, 14, 4608, 4608, 384, 384, 1, 1, 0),    # 29: = case25 as a 1x1 (same M, N, K)
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
