@@ -733,19 +733,34 @@ static int num_sms() {
   return n;
 }
 
-// N tile: the whole 16-aligned output width when it fits one tile; else the
-// width in {256, 128} that keeps the persistent grid busiest.
-int choose_bn(int cout_max, long M) {
+static int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
+// N tile: the whole 16-aligned output width when it fits one tile; else
+// {256, 128} from measured rules (tools/tile_sweep.sh over the R50 sweep)
+// and a wave-quantisation cost for the rest.  nk_max = K blocks of the
+// max-shape slice; pair tiles (cta_group::2) are used from 16 K blocks on.
+int choose_bn(int cout_max, long M, int nk_max) {
   const int c16 = (cout_max + 15) / 16 * 16;
   if (c16 <= 256) return c16;
-  const long mt = (M + TC_BM - 1) / TC_BM;
-  const long sms = num_sms();
+  static const int force = env_int("SSN_TC_FORCE_BN");  // tuning experiments only
+  if (force == 128 || force == 256) return force;
+  // <= 3 K blocks: the epilogue bounds the tile; narrower tiles drain faster
+  if (nk_max <= 3) return 128;
+  // 257..384 wide with real K (the 360-channel stage-3 layers): one wide tile
+  // plus a narrow one re-streams A less than three 128-wide tiles
+  if (cout_max <= 384 && nk_max >= 8) return 256;
+  const int cg = nk_max >= 16 ? 2 : 1;
+  const long mt = (M + TC_BM * cg - 1) / (TC_BM * cg);
+  const long slots = num_sms() / cg;
   auto cost = [&](int bn) {
     const long tiles = mt * ((cout_max + bn - 1) / bn);
-    const long waves = (tiles + sms - 1) / sms;
-    return waves * (bn + 64);
+    const long waves = (tiles + slots - 1) / slots;
+    return waves * (bn + (cg == 2 ? 128 : 64));
   };
-  return cost(128) < cost(256) ? 128 : 256;
+  return cost(256) <= cost(128) ? 256 : 128;
 }
 
 // Instances (BN_MAX, STAGES, K blocks per stage): the operand ring plus the
@@ -810,8 +825,12 @@ static bool resident_b(const ConvParams& p) {
 // epilogue dominates (1x1 256->256 +15%), so they need >= 16 K blocks.
 bool conv_tc_use_pairs(const ConvParams& p) {
   const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
-  return p.bn >= 128 && nk_max >= 16 && !resident_b(p) && !(tc_debug() & 16384) && p.act <= 2 &&
-         (p.cout_max & 7) == 0 && !p.ragged && !p.out_f32;
+  static const int min_nk = [] {  // tuning experiments only
+    const int v = env_int("SSN_TC_PAIR_MIN_NK");
+    return v > 0 ? v : 16;
+  }();
+  return p.bn >= 128 && nk_max >= min_nk && !resident_b(p) && !(tc_debug() & 16384) &&
+         p.act <= 2 && (p.cout_max & 7) == 0 && !p.ragged && !p.out_f32;
 }
 
 cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s) {

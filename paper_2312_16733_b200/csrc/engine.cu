@@ -33,7 +33,7 @@ namespace ssn {
 int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int bn);
 int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
                  int pad);
-int choose_bn(int cout_max, long M);
+int choose_bn(int cout_max, long M, int nk_max);
 bool conv_tc_use_pairs(const ConvParams& p);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
@@ -317,7 +317,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       if (bf && use_halo(e, o)) {
         CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
       } else if (bf && !o.depthwise) {
-        p.bn = choose_bn(o.cout_max, p.M);
+        p.bn = choose_bn(o.cout_max, p.M, o.k_max * o.k_max * ((t.cin_store + 63) / 64));
         p.cg2 = conv_tc_use_pairs(p);
         CUtensorMap wmap{};
         if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout,
@@ -1070,7 +1070,7 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
       CUDA_TRY(launch_conv_halo(p, wgt, cin_max, k * k, s));
       return;
     }
-    p.bn = choose_bn(cout_max, p.M);
+    p.bn = choose_bn(cout_max, p.M, k * k * ((cin_max + 63) / 64));
     // ragged slice, or SubnetNorm vectors the vector epilogue cannot load
     p.ragged = (cout & 7) != 0 || ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) != 0;
     p.cg2 = conv_tc_use_pairs(p);

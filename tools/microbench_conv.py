@@ -42,6 +42,9 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (16, 14, 14, 360, 360, 360, 360, 3, 1, 0),       # 27: case2 at n=16
     (256, 14, 14, 2048, 2048, 384, 384, 1, 1, 0),    # 28: bn128 pairs, tiled A (vs 25: im2col A)
     (256, 14, 14, 4608, 4608, 384, 384, 1, 1, 0),    # 29: = case25 as a 1x1 (same M, N, K)
+    (64, 14, 14, 360, 360, 1024, 1024, 1, 1, 0),     # 30: stage-3 expand, no residual
+    (64, 7, 7, 720, 720, 2048, 2048, 1, 1, 0),       # 31: stage-4 expand
+    (64, 14, 14, 1024, 1024, 360, 360, 1, 1, 0),     # 32: stage-3 reduce
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
