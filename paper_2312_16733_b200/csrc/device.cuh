@@ -156,6 +156,19 @@ struct InputParams {
   int ho, wo;
 };
 
+// Input staging fused with the bf16 im2col stem conv (3x3, stride 2, 3 input
+// channels, K = 27 padded to 32): raw images -> the conv's output directly.
+struct StemParams {
+  const void* raw;
+  void* y;
+  const OpDesc* const* row;
+  int op;                   // the stem conv's op index (WeightSlice cout, SubnetNorm)
+  const void* w;            // [cout_max][32] im2col-order weights
+  int n, h, w_, ho, wo;
+  int format;               // ssn_input_format
+  int act;
+};
+
 struct OpDims {
   int cin, cout, k, pad;
   const float* scale;
@@ -528,6 +541,17 @@ __device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t smem_addr, uint32_t
 __host__ __device__ __forceinline__ uint32_t umma_idesc_bf16(int n, int m = 128) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
          (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+// Legacy warp MMA (D += A B, m16n8k16, bf16 in / fp32 accumulate) for small
+// fused kernels (attention, the CNN stem) where tcgen05 setup would dominate.
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
+                                               const uint32_t b0, const uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {

@@ -42,6 +42,7 @@ bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_ma
 int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k);
 cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps, cudaStream_t s);
 cudaError_t launch_input(const InputParams& p, cudaStream_t s);
+cudaError_t launch_stem_conv(const StemParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
@@ -246,11 +247,32 @@ static bool use_halo(const ssn_engine* e, const OpSpec& o) {
   return halo_eligible(o.hin, o.win, o.k_max, o.stride, t.cin_store, o.cout_max);
 }
 
+static int tc_debug_flags() {  // SSN_TC_DEBUG & 65536: unfused stem (profiling only)
+  static const int v = [] {
+    const char* e = getenv("SSN_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// bf16 im2col stem conv `ci` (op 1 of both OFA CNN families) runs fused with
+// its input op (stem_conv_kernel): the input op launches nothing.
+static bool stem_fused(const ssn_engine* e, int ci) {
+  if (!e->bf16 || ci < 1 || ci >= static_cast<int>(e->net.ops.size())) return false;
+  const OpSpec& c = e->net.ops[ci];
+  const OpSpec& in = e->net.ops[ci - 1];
+  return c.kind == OP_CONV && c.tensor >= 0 && e->net.tensors[c.tensor].im2col_stem &&
+         in.kind == OP_INPUT && in.k_max == 3 && in.stride == 2 && in.cout_max == 32 &&
+         in.win <= 256 && c.cout_max <= 32 && (c.cout_max & 7) == 0 && c.res == S_NONE &&
+         !(tc_debug_flags() & 65536);
+}
+
 static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cudaStream_t s) {
   const OpSpec& o = e->net.ops[oi];
   const bool bf = e->bf16;
   switch (o.kind) {
     case OP_INPUT: {
+      if (stem_fused(e, oi + 1)) return 0;  // the stem conv reads the raw images
       InputParams p{};
       p.raw = e->d_raw;
       p.y = slot_ptr(e, o.out, map);
@@ -292,6 +314,24 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
     case OP_CONV:
     case OP_LINEAR: {
       const TensorSpec& t = e->net.tensors[o.tensor];
+      if (stem_fused(e, oi)) {
+        const OpSpec& in = e->net.ops[oi - 1];
+        StemParams sp{};
+        sp.raw = e->d_raw;
+        sp.y = slot_ptr(e, o.out, map);
+        sp.row = e->d_rowptr;
+        sp.op = oi;
+        sp.w = e->d_w + t.w_off;
+        sp.n = static_cast<int>(batch);
+        sp.h = in.hin;
+        sp.w_ = in.win;
+        sp.ho = o.hout;
+        sp.wo = o.wout;
+        sp.format = static_cast<int>(e->desc.input_format);
+        sp.act = o.act;
+        CUDA_TRY(launch_stem_conv(sp, s));
+        return 1;
+      }
       ConvParams p{};
       p.x = slot_ptr(e, o.in, map);
       p.y = slot_ptr(e, o.out, map);

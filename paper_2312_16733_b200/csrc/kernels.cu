@@ -156,6 +156,169 @@ __global__ void input_im2col_kernel(InputParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Input staging fused with the bf16 stem conv (3x3, stride 2, pad 1, 3
+// channels; both OFA stems): raw images -> SubnetNorm'd activations, no
+// im2col buffer.  One CTA = one output row (image, oh): the three input rows
+// it reads are normalised into shared memory as bf16 (1-px zero border),
+// each warp forms m16n8k16 A fragments (16 output pixels x 16 of the 27 window
+// values, zero past 27) straight from them, B = the [cout][32] im2col-order
+// weight slice in registers, fp32 accumulate; SubnetNorm + activation in
+// registers, the row is staged in shared memory and leaves as contiguous
+// 16-byte stores.  Replaces input_im2col3 + a K = 32 GEMM that wrote and
+// re-read a 32-channel im2col tensor (2 x 51 MB at bs64 x 224 px).
+constexpr int STEM_THREADS = 128;
+constexpr int STEM_MAXW = 256;                       // input width bound (engine checks)
+// staged input row (bf16): [5 unused][left zero pixel: 3][w pixels x 3][right zero pixel: 3],
+// pixel data 16-byte aligned at element 8
+constexpr int STEM_SROW = 8 + (STEM_MAXW + 1) * 3 + 5;
+constexpr int STEM_COUT = 32;                        // max stem width (4 n8 tiles)
+constexpr int STEM_RPC = 4;                          // output rows per CTA
+constexpr int STEM_IN_ROWS = 2 * STEM_RPC + 1;       // input rows they read
+
+__global__ void __launch_bounds__(STEM_THREADS) stem_conv_kernel(StemParams p) {
+  __shared__ __align__(16) __nv_bfloat16 s_in[STEM_IN_ROWS * STEM_SROW];
+  __shared__ __align__(16) __nv_bfloat16 s_out[(STEM_MAXW / 2 + 16) * STEM_COUT];
+  pdl_wait();
+  pdl_trigger();
+  const int rblk = (p.ho + STEM_RPC - 1) / STEM_RPC;
+  const int img = blockIdx.x / rblk, oh0 = (blockIdx.x - img * rblk) * STEM_RPC;
+  const int tid = threadIdx.x;
+  const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
+  if (tid < STEM_IN_ROWS * 6) {  // the zero border pixels
+    const int r = tid / 6, e = tid - r * 6;
+    s_in[r * STEM_SROW + (e < 3 ? 5 + e : 8 + 3 * p.w_ + e - 3)] = zero;
+  }
+  if (p.format == SSN_INPUT_U8_NHWC && (p.w_ * 3) % 16 == 0) {
+    // one 16-byte load per thread: row r, bytes 16q..16q+15 (pixels interleaved RGB)
+    const int vrow = p.w_ * 3 / 16;
+#pragma unroll 4
+    for (int idx = tid; idx < STEM_IN_ROWS * vrow; idx += STEM_THREADS) {
+      const int r = idx / vrow, q = idx - r * vrow;
+      const int ih = 2 * oh0 - 1 + r;
+      const bool ok = ih >= 0 && ih < p.h;
+      uint4 u = make_uint4(0u, 0u, 0u, 0u);
+      if (ok)
+        u = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(p.raw) +
+                                                 (static_cast<long>(img) * p.h + ih) * p.w_ * 3) + q);
+      const uint32_t wds[4] = {u.x, u.y, u.z, u.w};
+      uint32_t pk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t wd = wds[k >> 1] >> (16 * (k & 1));
+        const float v0 = ok ? (static_cast<float>(wd & 255u) - 128.f) * (1.f / 64.f) : 0.f;
+        const float v1 = ok ? (static_cast<float>((wd >> 8) & 255u) - 128.f) * (1.f / 64.f) : 0.f;
+        pk[k] = pack_bf16x2(v0, v1);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(s_in + r * STEM_SROW + 8 + 16 * q);
+      dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+  } else {
+    const int rowlen = p.w_ * 3;
+    for (int idx = tid; idx < STEM_IN_ROWS * rowlen; idx += STEM_THREADS) {
+      const int r = idx / rowlen, q = idx - r * rowlen;
+      const int px = q / 3, c = q - px * 3;
+      const int ih = 2 * oh0 - 1 + r;
+      float v = 0.f;
+      if (ih >= 0 && ih < p.h) {
+        if (p.format == SSN_INPUT_U8_NHWC) {
+          const uint8_t* src = static_cast<const uint8_t*>(p.raw);
+          v = (static_cast<float>(__ldg(src + ((static_cast<long>(img) * p.h + ih) * p.w_ + px) * 3 + c)) -
+               128.f) * (1.f / 64.f);
+        } else {
+          const float* src = static_cast<const float*>(p.raw);
+          v = __ldg(src + ((static_cast<long>(img) * 3 + c) * p.h + ih) * p.w_ + px);
+        }
+      }
+      s_in[r * STEM_SROW + 8 + q] = __float2bfloat16_rn(v);
+    }
+  }
+  const OpDims d = load_desc(p.row, nullptr, p.op);
+  const int cout = d.cout;  // active (WeightSlice), <= STEM_COUT, multiple of 8
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
+  // this thread's 8 window offsets: K index k = 16 ks + 8 hi + 2 tq + lo
+  int koff[8];
+  bool kok[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int k = (j >> 2) * 16 + ((j >> 1) & 1) * 8 + 2 * tq + (j & 1);
+    const int r = k / 9, sx = (k % 9) / 3, c = k % 3;
+    kok[j] = k < 27;
+    koff[j] = kok[j] ? r * STEM_SROW + 5 + 3 * sx + c : 0;  // window pixel (2 ow - 1 + sx)
+  }
+  // B fragments: column n = 8 nt + g of W^T, rows 2 tq (+1) and 2 tq + 8 (+1)
+  uint32_t b[4][2][2];
+  float sc[4][2], sh[4][2];
+  const uint32_t* wv = static_cast<const uint32_t*>(p.w);
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int n = 8 * nt + g;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      b[nt][ks][0] = n < cout ? __ldg(wv + (n * 32 + ks * 16 + 2 * tq) / 2) : 0u;
+      b[nt][ks][1] = n < cout ? __ldg(wv + (n * 32 + ks * 16 + 2 * tq + 8) / 2) : 0u;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = 8 * nt + 2 * tq + e;
+      sc[nt][e] = (d.scale && col < cout) ? __ldg(d.scale + col) : 1.f;
+      sh[nt][e] = (d.shift && col < cout) ? __ldg(d.shift + col) : 0.f;
+    }
+  }
+  __syncthreads();
+  const unsigned short* sin16 = reinterpret_cast<const unsigned short*>(s_in);
+  auto a_val = [&](int base, int j) -> uint32_t {
+    return kok[j] ? static_cast<uint32_t>(sin16[base + koff[j]]) : 0u;
+  };
+  const int mtiles = (p.wo + 15) / 16;
+  for (int rr = 0; rr < STEM_RPC; ++rr) {
+    const int oh = oh0 + rr;
+    if (oh >= p.ho) break;
+    const int rbase = 2 * rr * STEM_SROW;  // this output row's window starts at staged row 2 rr
+    for (int mt = warp; mt < mtiles; mt += STEM_THREADS / 32) {
+      const int ow0 = min(mt * 16 + g, p.wo - 1), ow1 = min(mt * 16 + g + 8, p.wo - 1);
+      float acc[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        uint32_t a[4];
+        const int j = ks * 4;
+        a[0] = a_val(rbase + 6 * ow0, j) | (a_val(rbase + 6 * ow0, j + 1) << 16);
+        a[1] = a_val(rbase + 6 * ow1, j) | (a_val(rbase + 6 * ow1, j + 1) << 16);
+        a[2] = a_val(rbase + 6 * ow0, j + 2) | (a_val(rbase + 6 * ow0, j + 3) << 16);
+        a[3] = a_val(rbase + 6 * ow1, j + 2) | (a_val(rbase + 6 * ow1, j + 3) << 16);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mma_bf16_16816(acc[nt], a, b[nt][ks][0], b[nt][ks][1]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ow = mt * 16 + g + 8 * h;
+        if (ow >= p.wo) continue;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int col = 8 * nt + 2 * tq;
+          if (col >= cout) continue;
+          const float o0 = act_apply(acc[nt][2 * h] * sc[nt][0] + sh[nt][0], p.act);
+          const float o1 = act_apply(acc[nt][2 * h + 1] * sc[nt][1] + sh[nt][1], p.act);
+          *reinterpret_cast<uint32_t*>(s_out + ow * cout + col) = pack_bf16x2(o0, o1);
+        }
+      }
+    }
+    __syncthreads();
+    // the output row is contiguous: wo * cout bf16 (16-byte multiple: cout % 8 == 0)
+    const int nvec = p.wo * cout / 8;
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) +
+                                          (static_cast<long>(img) * p.ho + oh) * p.wo * cout);
+    const uint4* src = reinterpret_cast<const uint4*>(s_out);
+    for (int i = tid; i < nvec; i += STEM_THREADS) dst[i] = src[i];
+    __syncthreads();  // s_out is rewritten by the next row
+  }
+}
+
+// ---------------------------------------------------------------------------
 // pooling, bf16 NHWC, 8 channels per thread
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
@@ -775,6 +938,12 @@ cudaError_t launch_input(const InputParams& p, cudaStream_t s) {
     return launch_pdl(input_im2col_kernel, dim3(grid_for(npix, 128)), dim3(128), 0, s, 1, p);
   return launch_pdl(input_kernel, dim3(grid_for(static_cast<long>(p.n) * p.h * p.w, 256)),
                     dim3(256), 0, s, 1, p);
+}
+
+cudaError_t launch_stem_conv(const StemParams& p, cudaStream_t s) {
+  if (p.w_ > STEM_MAXW || p.wo > STEM_MAXW / 2 + 16) return cudaErrorInvalidValue;
+  const int rblk = (p.ho + STEM_RPC - 1) / STEM_RPC;
+  return launch_pdl(stem_conv_kernel, dim3(p.n * rblk), dim3(STEM_THREADS), 0, s, 1, p);
 }
 
 // `max_c` bounds the grid for the largest subnet; surplus threads exit.

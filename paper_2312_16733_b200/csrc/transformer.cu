@@ -126,15 +126,6 @@ __global__ void token0_kernel(Token0Params p) {
 }
 
 // ---------------------------------------------------------------- attention
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
-                                               const uint32_t b0, const uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
 constexpr int ATT_S = 128, ATT_D = 64;
 constexpr int ATT_KLD = ATT_D + 8;   // K row stride (bf16), conflict-free fragment loads
 constexpr int ATT_VLD = ATT_S + 8;   // V^T row stride
