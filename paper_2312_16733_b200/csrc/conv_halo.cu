@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // PDL: upstream activations are read only after this
+  // PDL: the resident weights are static and load before griddepcontrol.wait
+  // (overlapping the predecessor's tail); activations only after it
   pdl_trigger();
   // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
   const bool prof = (p.dbg & 32) && blockIdx.x == 0;
@@ -140,6 +141,8 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                         (r + koff) * p.k_max + (s + koff), 0);
     }
     const CUtensorMap* amap = &dp->amap;
+    __syncwarp();
+    pdl_wait();
     int g = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int img = t / tpi;
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     // ============================================================ epilogue
     // Lane L of warp w drains TMEM row 32*(w%4) + L = one padded output
     // position; positions in the padding columns / past H are dropped.
+    pdl_wait();  // the residual is the predecessors' output
     const int quarter = warp & 3;
     const int group = (warp - 1) >> 2;
     const int p_row = quarter * 32 + lane;

@@ -201,9 +201,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (CG == 2) cluster_sync();  // the peer's barriers exist before any remote arrival / TMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // PDL: everything above touched only smem / TMEM / static descriptors; the
-  // predecessor's activations are read only after this
-  pdl_wait();
+  // PDL: everything above touched only smem / TMEM / static descriptors.
+  // Weights are static too: the producers issue the resident slice / the
+  // first ring stages' B boxes before griddepcontrol.wait, overlapping the
+  // predecessor's tail; activations (A, residual) are read only after it.
   pdl_trigger();
   // SSN_TC_DEBUG & 32: per-role cycle accounting of CTA 0 (profiling only)
   const bool prof = (p.dbg & 32) && blockIdx.x == 0;
@@ -243,6 +244,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
+    // B of the first tile's leading ring stages, ahead of the PDL wait
+    const int npre = (KPS == 1 && !RESB && !(p.dbg & 8)) ? min(STAGES, nk) : 0;
+    const uint32_t a_tx1 = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
+    const uint32_t b_tx1 = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
+    if (npre && leader) {
+      const int n0 = (unit0 % nt) * bn + static_cast<int>(rank) * (bn / CG);
+      int tr = 0, ts = 0, cb = 0;
+      for (int kb = 0; kb < npre; ++kb) {
+        if (kb % TC_NPROD == pidx) {
+          if (rank == 0) mbar_arrive_expect_tx(&full[kb], a_tx1 + b_tx1);
+          uint8_t* dst = sB + kb * C::B_BYTES;
+          if (CG == 2)
+            tma2_load_3d(dst, &wmap, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+          else
+            tma_load_3d(dst, &wmap, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+        }
+        if (++cb == cblocks) {
+          cb = 0;
+          if (++ts == ka) {
+            ts = 0;
+            ++tr;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    pdl_wait();
     int g = 0;  // stage counter (ring position)
     for (int t = unit0; t < tiles; t += ustep) {
       const int m0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM;  // this CTA's rows
@@ -277,7 +305,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&empty[s], ph ^ 1);
         }
         const int nsub = min(KPS, nk - kb);
-        if (leader && rank == 0) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
+        const bool pre = g < npre;  // B already in flight, barrier armed
+        if (leader && rank == 0 && !pre) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
           const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
           const uint32_t tx = nsub * (a_tx + (RESB ? 0u : b_tx));
@@ -301,7 +330,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                               static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
               }
             }
-            if (leader && !RESB && !(p.dbg & 8)) {
+            if (leader && !RESB && !(p.dbg & 8) && !pre) {
               uint8_t* dst = sB + (s * KPS + j) * C::B_BYTES;
               if (CG == 2)
                 tma2_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
@@ -332,6 +361,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // quarter) split the work (see `stripe`).  Software-pipelined: the
     // SubnetNorm row and residual of the warp's NEXT chunk are in flight
     // while this chunk is drained.
+    pdl_wait();  // the residual is the predecessors' output
     const int ew = warp - TC_EPI_WARP0;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warps 1-4, 5-8)
     const int group = ew >> 2;     // chunk stripe this warp drains
