@@ -768,20 +768,31 @@ static int env_int(const char* name) {
   return e ? atoi(e) : 0;
 }
 
-// N tile: the whole 16-aligned output width when it fits one tile; else
-// {256, 128} from measured rules (tools/tile_sweep.sh over the R50 sweep)
-// and a wave-quantisation cost for the rest.  nk_max = K blocks of the
-// max-shape slice; pair tiles (cta_group::2) are used from 16 K blocks on.
+// N tile: the whole 16-aligned output width when it fits one tile.  Wider
+// slices take any 16-multiple <= 256 (the kernel's N is a runtime value):
+// the per-SM operand feed, not the MMA, bounds these layers, so the width
+// trades A re-streaming (narrow) against idle SMs (wide, few tiles).  The
+// table is measured (tools/tile_sweep.sh: per-op device time summed over the
+// {min, mid, max} sweep, N in {128..256}); other shapes use a wave cost.
+// nk_max = K blocks of the max-shape slice; pairs from 16 K blocks on.
 int choose_bn(int cout_max, long M, int nk_max) {
   const int c16 = (cout_max + 15) / 16 * 16;
   if (c16 <= 256) return c16;
   static const int force = env_int("SSN_TC_FORCE_BN");  // tuning experiments only
-  if (force == 128 || force == 256) return force;
-  // <= 3 K blocks: the epilogue bounds the tile; narrower tiles drain faster
-  if (nk_max <= 3) return 128;
-  // 257..384 wide with real K (the 360-channel stage-3 layers): one wide tile
-  // plus a narrow one re-streams A less than three 128-wide tiles
-  if (cout_max <= 384 && nk_max >= 8) return 256;
+  if (force >= 16 && force <= 256 && force % 16 == 0) return force;
+  if (cout_max <= 384) {                 // e.g. 360: 3x3 (54 kb), 1024->360, 512->360
+    if (nk_max >= 32) return 144;
+    if (nk_max >= 8) return 224;
+    return 128;
+  }
+  if (cout_max <= 512) return nk_max <= 4 ? 192 : 256;   // 176/256 -> 512 at 28 px
+  if (cout_max <= 768) {                 // 720: 3x3 (108 kb), 2048->720, 1024->720
+    if (nk_max >= 64) return 144;
+    if (nk_max >= 24) return 160;
+    return 192;
+  }
+  if (cout_max <= 1024) return nk_max >= 8 ? 256 : 192;
+  if (cout_max <= 2048 && nk_max >= 12) return 192;
   const int cg = nk_max >= 16 ? 2 : 1;
   const long mt = (M + TC_BM * cg - 1) / (TC_BM * cg);
   const long slots = num_sms() / cg;
