@@ -36,6 +36,7 @@
 //    serves every subnet; the tile count follows cout_a on the device.
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 
 #include "device.cuh"
 
@@ -155,10 +156,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int mt = (p.M + TC_BM * CG - 1) / (TC_BM * CG);  // CG = 2: 256-row pair tiles
   const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
   const int tiles = mt * nt;
+  const int S = p.splits > 1 ? p.splits : 1;  // split-K: work unit u = (tile u / S, K range u % S)
+  const int units = tiles * S;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const int unit0 = static_cast<int>(blockIdx.x) / CG;     // this CTA's (pair's) first tile
   const int ustep = static_cast<int>(gridDim.x) / CG;
-  if (unit0 >= tiles) return;  // both CTAs of a pair agree
+  if (unit0 >= units) return;  // both CTAs of a pair agree
   // Epilogue work split: wide tiles (>= TC_EPI_GROUPS 32-column chunks) are
   // striped chunk-wise across all groups; narrow ones go whole to one group
   // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // B of the first tile's leading ring stages, ahead of the PDL wait
-    const int npre = (KPS == 1 && !RESB && !(p.dbg & 8)) ? min(STAGES, nk) : 0;
+    const int npre = (KPS == 1 && !RESB && !(p.dbg & 8) && S == 1) ? min(STAGES, nk) : 0;
     const uint32_t a_tx1 = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
     const uint32_t b_tx1 = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
     if (npre && leader) {
@@ -272,7 +275,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncwarp();
     pdl_wait();
     int g = 0;  // stage counter (ring position)
-    for (int t = unit0; t < tiles; t += ustep) {
+    for (int u = unit0; u < units; u += ustep) {
+      const int t = u / S, z = u - t * S;
+      const int kb_lo = z * nk / S, kb_hi = (z + 1) * nk / S;
       const int m0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM;  // this CTA's rows
       const int n0 = (t % nt) * bn + static_cast<int>(rank) * (bn / CG);      // this CTA's B rows
       const int img = m0 / hwo;
@@ -280,8 +285,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int oh = rem / p.wo;
       const int ow = rem - oh * p.wo;
       const int w0 = ow * p.stride - pad, h0 = oh * p.stride - pad;
-      int tr = 0, ts = 0, cb = 0;
-      for (int kb = 0; kb < nk; kb += KPS, ++g) {
+      int cb = kb_lo % cblocks, ts = (kb_lo / cblocks) % ka, tr = kb_lo / cblocks / ka;
+      for (int kb = kb_lo; kb < kb_hi; kb += KPS, ++g) {
         if (g % TC_NPROD != pidx) {  // another producer's block: advance the (tap, channel) walk
 #pragma unroll
           for (int j = 0; j < KPS; ++j) {
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         } else {
           mbar_wait(&empty[s], ph ^ 1);
         }
-        const int nsub = min(KPS, nk - kb);
+        const int nsub = min(KPS, kb_hi - kb);
         const bool pre = g < npre;  // B already in flight, barrier armed
         if (leader && rank == 0 && !pre) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
@@ -448,15 +453,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int c = c0;
     EpiIn cur;  // this chunk's SubnetNorm row + residual (no register prefetch:
                 // 12 warps hide the latency, and 512 threads cap registers at 128)
-    while (t < tiles) {
+    while (t < units) {
+      const int tt = t / S;  // tile of work unit t
       int tn = t, cn = c + c_step, inx = i;
-      if (cn >= chunks_of(t)) {
+      if (cn >= chunks_of(tt)) {
         cn = c0;
         inx = i + i_step;
         tn = t + i_step * ustep;
       }
       // operands of this chunk, issued before the accumulator wait / TMEM load
-      if (!(p.dbg & 1) && c < chunks_of(t)) fetch(cur, t, c);
+      if (!(p.dbg & 1) && S == 1 && c < chunks_of(tt)) fetch(cur, tt, c);
       const int a = i % NACC;
       if (c == c0) {
         if (prof) {
@@ -468,7 +474,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         tc_fence_after();
       }
-      if (c >= chunks_of(t)) {  // no chunk of this tile for this group
+      if (c >= chunks_of(tt)) {  // no chunk of this tile for this group
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_tempty(a);
@@ -477,9 +483,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         i = inx;
         continue;
       }
-      const int m0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
+      const int m0 = (tt / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
       const int cc = c * 32;
-      const int col = (t % nt) * bn + cc + seg * 8;
+      const int col = (tt % nt) * bn + cc + seg * 8;
       const bool colok = col < d.cout && cc + seg * 8 < bn;
       const int nv = colok ? min(8, d.cout - col) : 0;
       const bool vec = EPI != 2 || (nv == 8 && (d.cout & 7) == 0);
@@ -514,6 +520,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const float4 lo = sp[0], hi = sp[1];
           o[r4][0] = lo.x; o[r4][1] = lo.y; o[r4][2] = lo.z; o[r4][3] = lo.w;
           o[r4][4] = hi.x; o[r4][5] = hi.y; o[r4][6] = hi.z; o[r4][7] = hi.w;
+        }
+        if (S > 1) {  // split-K partial: raw fp32 into this K range's workspace slice
+          float* wz = p.ws + static_cast<size_t>(t - tt * S) * p.M * d.cout;
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4) {
+            const int m = m0 + rsub + 8 * r4;
+            if (m < p.M) {
+              float4* wp = reinterpret_cast<float4*>(wz + static_cast<size_t>(m) * d.cout + col);
+              wp[0] = make_float4(o[r4][0], o[r4][1], o[r4][2], o[r4][3]);
+              wp[1] = make_float4(o[r4][4], o[r4][5], o[r4][6], o[r4][7]);
+            }
+          }
+          if (prof) w_wait2 += clock64() - tsec;
+          __syncwarp();
+          t = tn;
+          c = cn;
+          i = inx;
+          continue;
         }
 #pragma unroll
         for (int r4 = 0; r4 < 4; ++r4)
@@ -600,7 +624,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
     }
     int g = 0, i = 0;
-    for (int t = unit0; t < tiles; t += ustep, ++i) {
+    for (int u = unit0; u < units; u += ustep, ++i) {
+      const int z = u % S;
+      const int kb_lo = z * nk / S, kb_hi = (z + 1) * nk / S;
       const int a = i % NACC;
       const uint32_t use = static_cast<uint32_t>(i / NACC);
       if (prof) {
@@ -612,7 +638,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_after();
       const uint32_t acc = tmem + a * BN_MAX;
-      for (int kb = 0; kb < nk; kb += KPS, ++g) {
+      for (int kb = kb_lo; kb < kb_hi; kb += KPS, ++g) {
         const int s = g % STAGES;
         const uint32_t ph = (g / STAGES) & 1;
         if (prof) {
@@ -623,7 +649,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&full[s], ph);
         }
         tc_fence_after();
-        const int nsub = min(KPS, nk - kb);
+        const int nsub = min(KPS, kb_hi - kb);
 #pragma unroll
         for (int j = 0; j < KPS; ++j) {
           if (j < nsub) {
@@ -636,20 +662,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (CG == 2)
                 tc2_mma_bf16_elect(acc, ad + static_cast<uint64_t>(kk * 2),
                                    bd + static_cast<uint64_t>(kk * 2), idesc,
-                                   ((kb + j) | kk) != 0 ? 1u : 0u);
+                                   ((kb - kb_lo + j) | kk) != 0 ? 1u : 0u);
               else
                 tc_mma_bf16_elect(acc, ad + static_cast<uint64_t>(kk * 2),
                                   bd + static_cast<uint64_t>(kk * 2), idesc,
-                                  ((kb + j) | kk) != 0 ? 1u : 0u);
+                                  ((kb - kb_lo + j) | kk) != 0 ? 1u : 0u);
             }
           }
         }
         if (CG == 2) {  // free the stage / publish the accumulator in BOTH CTAs
           tc2_commit_mc_elect(&empty[s]);
-          if (kb + KPS >= nk) tc2_commit_mc_elect(&tfull[a]);
+          if (kb + KPS >= kb_hi) tc2_commit_mc_elect(&tfull[a]);
         } else {
           tc_commit_elect(&empty[s]);
-          if (kb + KPS >= nk) tc_commit_elect(&tfull[a]);
+          if (kb + KPS >= kb_hi) tc_commit_elect(&tfull[a]);
         }
         __syncwarp();
       }
@@ -667,6 +693,65 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tmem2_dealloc(tmem, C::TMEM_COLS);
     else
       tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// Split-K finish: workspace slice z holds K range z's raw sum of every (row,
+// column) of the active slice; add the slices in fixed order (deterministic,
+// no atomics) and apply conv_tc's fused epilogue (SubnetNorm, residual
+// before / after the activation).  8 columns per thread, 16-byte accesses.
+__global__ void __launch_bounds__(256) conv_finish_kernel(const __grid_constant__ ConvParams p) {
+  pdl_wait();
+  pdl_trigger();
+  const OpDims d = load_desc(p.row, p.fixed, p.op);
+  const int g8 = d.cout / 8;
+  const long n = static_cast<long>(p.M) * g8;
+  const size_t slice = static_cast<size_t>(p.M) * d.cout;
+  for (long i = blockIdx.x * 256L + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * 256) {
+    const long m = i / g8;
+    const int c = static_cast<int>(i - m * g8) * 8;
+    float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int z = 0; z < p.splits; ++z) {
+      const float4* wp = reinterpret_cast<const float4*>(p.ws + z * slice + m * d.cout + c);
+      const float4 a0 = wp[0], a1 = wp[1];
+      o[0] += a0.x; o[1] += a0.y; o[2] += a0.z; o[3] += a0.w;
+      o[4] += a1.x; o[5] += a1.y; o[6] += a1.z; o[7] += a1.w;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      o[q] = o[q] * (d.scale ? __ldg(d.scale + c + q) : 1.f) + (d.shift ? __ldg(d.shift + c + q) : 0.f);
+    float r[8];
+    if (p.res) {
+      const uint4 rv = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.res) +
+                                                           m * d.cout + c));
+      const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(rh[q]);
+        r[2 * q] = f.x;
+        r[2 * q + 1] = f.y;
+      }
+      if (!p.res_post)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] += r[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = act_apply(o[q], p.act);
+    if (p.res && p.res_post)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] += r[q];
+    if (p.out_f32) {
+      float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + m * d.cout + c);
+      yp[0] = make_float4(o[0], o[1], o[2], o[3]);
+      yp[1] = make_float4(o[4], o[5], o[6], o[7]);
+    } else {
+      uint4 pk;
+      pk.x = pack_bf16x2(o[0], o[1]);
+      pk.y = pack_bf16x2(o[2], o[3]);
+      pk.z = pack_bf16x2(o[4], o[5]);
+      pk.w = pack_bf16x2(o[6], o[7]);
+      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + m * d.cout + c) = pk;
+    }
   }
 }
 
@@ -831,7 +916,7 @@ template <int BN_MAX, int STAGES, int KPS, int RESB, int CG = 1>
 static cudaError_t launch_impl(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s) {
   using C = TcCfg<BN_MAX, STAGES, KPS, RESB, CG>;
   const long tiles = static_cast<long>((p.M + TC_BM * CG - 1) / (TC_BM * CG)) *
-                     ((p.cout_max + p.bn - 1) / p.bn);
+                     ((p.cout_max + p.bn - 1) / p.bn) * (p.splits > 1 ? p.splits : 1);
   void (*fn)(ConvParams, CUtensorMap) =
       (p.act > 2 || (p.cout_max & 7) != 0 || p.ragged) ? conv_tc_kernel<BN_MAX, STAGES, KPS, 2, RESB, CG>
       : p.act == 2                                      ? conv_tc_kernel<BN_MAX, STAGES, KPS, 1, RESB, CG>
@@ -874,7 +959,46 @@ bool conv_tc_use_pairs(const ConvParams& p) {
          p.act <= 2 && (p.cout_max & 7) == 0 && !p.ragged && !p.out_f32;
 }
 
+cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s);
+
+// Split-K for layers with few output tiles (small batch, 7-14 px stages):
+// the K range of each tile is split over idle SMs, partial sums meet in a
+// fp32 workspace (one slice per K range), conv_finish_kernel adds them and
+// applies the epilogue.  The
+// caller (engine) then encodes the weight map for single-CTA tiles.
+int conv_tc_splits(const ConvParams& p) {
+  // (not the classifier: one 64-row tile of a short-K GEMM gains less than
+  // the extra launch costs)
+  if (!p.ws || p.ragged || p.out_f32 || (p.cout_max & 7) != 0 || resident_b(p) ||
+      (tc_debug() & 131072))
+    return 1;
+  const long tiles = static_cast<long>((p.M + TC_BM - 1) / TC_BM) * ((p.cout_max + p.bn - 1) / p.bn);
+  const int nk_max = p.k_max * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
+  // worth a second kernel only when each split still streams >= 8 K blocks
+  // and the unsplit tile is long (>= 32 K blocks, ~10 us of operand feed)
+  if (tiles * 2 > num_sms() || nk_max < 32) return 1;
+  long sp = num_sms() / tiles;
+  sp = std::min<long>(sp, nk_max / 8);
+  sp = std::min<long>(sp, 16);
+  sp = std::min<long>(sp, SSN_SPLIT_WS_FLOATS / (static_cast<long>(p.M) * p.cout_max));
+  return sp >= 2 ? static_cast<int>(sp) : 1;
+}
+
+cudaError_t launch_conv_finish(const ConvParams& p, cudaStream_t s) {
+  const long n = static_cast<long>(p.M) * (p.cout_max / 8);
+  const long g = std::min<long>((n + 255) / 256, static_cast<long>(num_sms()) * 8);
+  return launch_pdl(conv_finish_kernel, dim3(static_cast<unsigned>(g > 0 ? g : 1)), dim3(256), 0, s, 1, p);
+}
+
 cudaError_t launch_conv_tc(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s) {
+  if (p_in.splits > 1) {
+    cudaError_t e = launch_conv_tc_main(p_in, wmap, s);
+    return e != cudaSuccess ? e : launch_conv_finish(p_in, s);
+  }
+  return launch_conv_tc_main(p_in, wmap, s);
+}
+
+cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap, cudaStream_t s) {
   const int dbg = tc_debug();
   ConvParams p = p_in;
   p.dbg = dbg;

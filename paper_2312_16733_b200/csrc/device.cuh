@@ -96,6 +96,10 @@ struct SEParams {
 };
 
 // Static (graph-baked) parameters of one conv op.
+// split-K workspace: fp32 [splits][M][cout_a]; splits x tiles <= num_sms
+// output tiles of <= 128 x 256 (conv_tc_splits)
+constexpr long SSN_SPLIT_WS_FLOATS = 148L * 128 * 256;
+
 struct ConvParams {
   const void* x;      // NHWC, stride = desc.cin
   void* y;            // NHWC, stride = desc.cout
@@ -113,6 +117,10 @@ struct ConvParams {
   int cg2;            // weight map boxes hold bn/2 rows: 2-CTA pair tiles (conv_tc CG = 2)
   // halo kernel (conv_halo.cu): resident weight box rows / K chunks, A ring depth
   int hb_rows, hb_chunks, h_stages;
+  // split-K (conv_tc): `splits` K ranges per tile write raw fp32 sums to
+  // `ws` ([splits][M][cout_a]); conv_finish_kernel adds them + the epilogue
+  int splits;
+  float* ws;
   int dbg;            // profiling knob (SSN_TC_DEBUG): 1 = epilogue skips global
                       // memory, 2 = no MMA issued (bottleneck isolation only)
 };

@@ -35,6 +35,7 @@ int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, 
                  int pad);
 int choose_bn(int cout_max, long M, int nk_max);
 bool conv_tc_use_pairs(const ConvParams& p);
+int conv_tc_splits(const ConvParams& p);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t init_conv_halo();
@@ -128,6 +129,7 @@ struct ssn_engine {
   Net net;  // max-shape plan
   bool bf16 = true;
   uint8_t* d_w = nullptr;
+  float* d_ws = nullptr;  // split-K partial sums (bf16 engines)
   std::vector<std::vector<float>> gamma, beta;  // host copies for SubnetNorm folding
   std::vector<SubnetState> subs;
   const OpDesc** d_rowptr = nullptr;
@@ -358,12 +360,15 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
         CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
       } else if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M, o.k_max * o.k_max * ((t.cin_store + 63) / 64));
-        p.cg2 = conv_tc_use_pairs(p);
+        p.ws = e->d_ws;
+        p.splits = conv_tc_splits(p);
+        p.cg2 = p.splits > 1 ? 0 : conv_tc_use_pairs(p);
         CUtensorMap wmap{};
         if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout,
                             p.cg2 ? p.bn / 2 : p.bn) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
         CUDA_TRY(launch_conv_tc(p, wmap, s));
+        return p.splits > 1 ? 2 : 1;  // + conv_finish_kernel
       } else if (bf) {
         CUDA_TRY(launch_dw_bf16(p, s));
       } else {
@@ -750,6 +755,9 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     for (int i = 0; i < NBUF; ++i) CUDA_TRY(cudaMalloc(&e->bufs[i], e->buf_bytes));
     e->raw_img_bytes = raw_image_bytes(*desc);
     CUDA_TRY(cudaMalloc(&e->d_raw, e->raw_img_bytes * desc->max_batch));
+    if (e->bf16) {
+      CUDA_TRY(cudaMalloc(&e->d_ws, SSN_SPLIT_WS_FLOATS * sizeof(float)));
+    }
     CUDA_TRY(cudaMemset(e->d_raw, 0, e->raw_img_bytes * desc->max_batch));
     for (int k = 0; k < 2; ++k) {
       CUDA_TRY(cudaMalloc(&e->d_stage[k], e->raw_img_bytes * desc->max_batch));
@@ -786,6 +794,7 @@ void ssn_destroy(ssn_engine* e) {
   }
   for (int i = 0; i < NBUF; ++i) cudaFree(e->bufs[i]);
   cudaFree(e->d_raw);
+  cudaFree(e->d_ws);
   for (int k = 0; k < 2; ++k) {
     cudaFree(e->d_stage[k]);
     if (e->stage_ready[k]) cudaEventDestroy(e->stage_ready[k]);

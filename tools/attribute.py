@@ -56,7 +56,14 @@ for n in names:
     per_fwd.append((n, ops))
 # the last len(names) forwards in the list are the measured step
 need = sum(len(ops) for _, ops in per_fwd)
-ops_launches = [l for l in launches if "set_row" not in l[0]]
+ops_launches = []
+for l in launches:
+    if "set_row" in l[0]:
+        continue
+    if "conv_finish_kernel" in l[0] and ops_launches:  # split-K tail of the previous conv
+        ops_launches[-1] = (ops_launches[-1][0], ops_launches[-1][1] + l[1])
+        continue
+    ops_launches.append(l)
 ops_launches = ops_launches[-need:]
 out, k = [], 0
 for n, ops in per_fwd:
