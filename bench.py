@@ -379,6 +379,7 @@ def live_roofline(eng, desc, cfgs, B, peaks, ssn):
     tot_f = tot_t = tot_b = 0.0
     roof_t = meas_t = 0.0
     conv_t = all_t = 0.0
+    conv_roof_t = 0.0
     n_conv = 0
     largest = None
     for sid, cfg in enumerate(cfgs):
@@ -392,11 +393,13 @@ def live_roofline(eng, desc, cfgs, B, peaks, ssn):
             all_t += t
             f = p["flops"] * B
             byts = p["bytes"] * B + p["weight_bytes"]
-            roof_t += max(f / (peaks["tc_sust"] * 1e12), byts / (peaks["hbm"] * 1e9))
+            op_roof = max(f / (peaks["tc_sust"] * 1e12), byts / (peaks["hbm"] * 1e9))
+            roof_t += op_roof
             meas_t += t
             if r["kind"] in (1, 5):
                 n_conv += 1
                 conv_t += t
+                conv_roof_t += op_roof
                 tot_f += f
                 tot_b += byts
                 tot_t += t
@@ -438,6 +441,8 @@ def live_roofline(eng, desc, cfgs, B, peaks, ssn):
         "max_subnet_conv_tflops": round(largest["f"] / largest["t"] / 1e12, 1) if largest else None,
         "max_subnet_weightslice_gemm": big,
         "whole_net_roofline_frac": round(roof_t / meas_t, 4),
+        # each conv launch against ITS bound (tensor or HBM), summed over the sweep
+        "conv_roofline_frac_own_bound": round(conv_roof_t / conv_t, 4),
         "note": "achieved = algorithmic 2*MAC of active WeightSlice extents / summed per-launch "
                 "CUDA-event time; whole_net = sum_op max(flops/tc, bytes/hbm) / sum_op measured",
     }
