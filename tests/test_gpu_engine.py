@@ -268,3 +268,26 @@ def test_bert_bf16_parity(bert, name):
     assert e_emu <= 2e-2
     assert e_ref <= 4e-2
     argmax_agree(got, emu, tol=4 * e_emu * np.abs(emu).max())
+
+
+def test_ofa_resnet50_split_k_matches_full_batch(gpu):
+    """At 224 px, bs1 runs the late-stage convs split-K (few output tiles,
+    per-split fp32 slices + conv_finish_kernel) while bs64 runs them unsplit:
+    image 0 must agree across the two paths, and each path is bit-stable."""
+    desc = ssn.make_desc(ssn.FAMILY_OFA_RESNET50, ssn.DTYPE_BF16, image_size=224,
+                         num_classes=1000, max_batch=64, seed=SEED,
+                         input_format=ssn.INPUT_U8_NHWC)
+    eng = ssn.Engine(desc)
+    try:
+        eng.register_subnet(0, ssn.ofa_resnet50_preset("max"))
+        eng.prepare([1, 64])
+        eng.actuate(0)
+        rng = np.random.default_rng(SEED)
+        x = rng.integers(0, 256, size=(64, 224, 224, 3), dtype=np.uint8)
+        full = eng.infer(x, 64, 64)
+        one = eng.infer(x[:1], 1, 1)
+        np.testing.assert_array_equal(one, eng.infer(x[:1], 1, 1))
+        assert rel(one[0], full[0]) < 2e-2, rel(one[0], full[0])
+        assert one[0].argmax() == full[0].argmax()
+    finally:
+        eng.close()
