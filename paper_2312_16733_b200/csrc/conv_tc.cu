@@ -893,7 +893,8 @@ int choose_bn(int cout_max, long M, int nk_max) {
 // 36 KB epilogue staging fill the 227 KB of shared memory; resident-B
 // instances trade ring stages for the 96 KB weight block.
 #define SSN_TC_INSTANCES(X) X(64, 7, 1, 0, 1) X(128, 5, 1, 0, 1) X(256, 3, 1, 0, 1) \
-  X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2) X(128, 7, 1, 0, 2)
+  X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2) X(128, 7, 1, 0, 2) \
+  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2)
 
 cudaError_t init_conv_tc() {
 #define SSN_TC_ATTR(BN, ST, KPS, RB, CG)                                                  \
@@ -1010,6 +1011,10 @@ cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap,
     if (resb) return launch_impl<128, 4, 1, 1>(p, wmap, s);
     if (p.cg2) return launch_impl<128, 7, 1, 0, 2>(p, wmap, s);  // bn == 128 pair tiles
     return launch_impl<128, 5, 1, 0>(p, wmap, s);
+  }
+  if (p.bn <= 192 && !resb && !(dbg & 524288)) {  // 144..192-wide tiles: deeper rings than BN 256
+    if (p.cg2) return launch_impl<192, 6, 1, 0, 2>(p, wmap, s);
+    return launch_impl<192, 4, 1, 0>(p, wmap, s);
   }
   if (resb) return launch_impl<256, 4, 1, 1>(p, wmap, s);
   // bn > 128: pair tiles (cta_group::2) unless SSN_TC_DEBUG & 16384
