@@ -70,12 +70,20 @@ constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
 // ring.  Re-streaming B per tile was ~40% of such a layer's time
 // (SSN_TC_DEBUG=8 isolation) because every tile re-read the same weights.
 constexpr int TC_RB_BYTES = 96 * 1024;
+// RESB = 2: a 64 KB resident slice plus the residual ring — per epilogue
+// group two 8 KB slots of {128 rows x 32 columns} bf16, filled by warp 3
+// with TMA one chunk ahead of the group (the residual was the epilogue's
+// latency bound: one 16-byte register load per lane per row in flight).
+constexpr int TC_RB2_BYTES = 64 * 1024;
+constexpr int TC_RR_SLOT = 128 * 32 * 2;
+constexpr int TC_RR_SLOTS = 2 * 3;
 
 template <int BN_MAX, int STAGES, int KPS, int RESB = 0, int CG = 1>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN_MAX / CG * TC_BK * 2;  // CG = 2: this CTA's half of N
-  static constexpr int RB_BLOCKS = RESB ? TC_RB_BYTES / B_BYTES : 0;
+  static constexpr int RB = RESB == 2 ? TC_RB2_BYTES : (RESB ? TC_RB_BYTES : 0);
+  static constexpr int RR = RESB == 2 ? TC_RR_SLOT * TC_RR_SLOTS : 0;
   static constexpr int STAGE_BYTES = KPS * (A_BYTES + (RESB ? 0 : B_BYTES));
   // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
   // (max 4), so the MMA can run several tiles ahead of the epilogue.
@@ -84,8 +92,8 @@ struct TcCfg {
   // else a group could pass a stale mbarrier phase of an older use.)
   static constexpr int NACC = BN_MAX <= 64 ? 3 : (512 / BN_MAX > 4 ? 4 : 512 / BN_MAX);
   static constexpr int TMEM_COLS = NACC * BN_MAX <= 256 ? 256 : 512;  // power-of-2 allocation
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + (RESB ? TC_RB_BYTES : 0) +
-                              TC_STG_BYTES + (2 * STAGES + 2 * NACC + 1) * 8 + 16;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + RB + RR + TC_STG_BYTES +
+                              (2 * STAGES + 2 * NACC + 1 + 2 * TC_RR_SLOTS) * 8 + 16;
   static_assert(SMEM <= 232448, "operand ring exceeds 227 KB of shared memory");
 };
 
@@ -141,14 +149,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                 // [STAGES][KPS] A boxes
   uint8_t* sB = smem + STAGES * KPS * C::A_BYTES;     // [STAGES][KPS] B boxes | RESB: [nk] blocks
-  uint8_t* epi_base = smem + STAGES * C::STAGE_BYTES + (RESB ? TC_RB_BYTES : 0);
+  uint8_t* sR = smem + STAGES * C::STAGE_BYTES + C::RB;  // RESB = 2: residual ring
+  uint8_t* epi_base = sR + C::RR;
   float* epi_stage = reinterpret_cast<float*>(epi_base);
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_base + TC_STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [NACC]
   uint64_t* tempty = tfull + NACC;   // [NACC]
   uint64_t* bfull = tempty + NACC;  // RESB: the resident weight slice landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* rfull = bfull + 1;      // RESB = 2: [group * 2 + slot]
+  uint64_t* rempty = rfull + TC_RR_SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + TC_RR_SLOTS);
 
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
@@ -189,6 +200,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tempty[a], (stripe ? TC_EPI_WARPS : 4) * CG);
     }
     mbar_init(bfull, 1);
+    for (int r = 0; r < TC_RR_SLOTS; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], 4);  // the group's four warps
+    }
     fence_mbar_init();
     tma_prefetch(&wmap);
     tma_prefetch(&dp->amap);
@@ -214,14 +229,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   long long w_wait = 0, w_wait2 = 0;
   const long long t_begin = prof ? clock64() : 0;
 
-  if (warp == TC_PROD_WARP || warp == TC_PROD2_WARP || warp == TC_PROD3_WARP) {
+  constexpr int NPROD = RESB == 2 ? 2 : TC_NPROD;  // RESB = 2: warp 3 streams the residual
+  if (RESB == 2 && warp == TC_PROD3_WARP) {
+    // ============================================================ residual ring
+    // Chunk c of every tile goes to group c % 3's ring (the group drains
+    // its chunks in this same order), slot = that group's sequence % 2.
+    static_assert(RESB != 2 || CG == 1, "residual ring: single-CTA tiles");
+    pdl_wait();  // the residual is the predecessors' output
+    const bool leader = elect_one();
+    const int nchunk = (bn + 31) / 32;
+    int kseq[3] = {0, 0, 0};
+    for (int t = unit0; t < tiles; t += ustep) {
+      const int m0 = (t / nt) * TC_BM;
+      const int left = d.cout - (t % nt) * bn;
+      const int nch = min(nchunk, (left + 31) / 32);
+      for (int c = 0; c < nch; ++c) {
+        const int g3 = c % 3;
+        const int k = kseq[g3]++;
+        const int slot = g3 * 2 + (k & 1);
+        mbar_wait(&rempty[slot], ((k >> 1) & 1) ^ 1);
+        if (leader) {
+          mbar_arrive_expect_tx(&rfull[slot], TC_RR_SLOT);
+          tma_load_2d(sR + slot * TC_RR_SLOT, &dp->rmap, &rfull[slot], (t % nt) * bn + c * 32, m0);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == TC_PROD_WARP || warp == TC_PROD2_WARP || warp == TC_PROD3_WARP) {
     // ============================================================ producers
     // K block g (ring position) belongs to producer g % TC_NPROD, which loads
     // its A (activations) and B (weights) boxes; warp 0 also preloads the
     // resident B.  Safe against mbarrier phase aliasing: a producer reaching
     // g has filled g - TC_NPROD, which needed g - TC_NPROD - STAGES released,
     // so g - 2 * STAGES was released too (TC_NPROD <= STAGES).
-    static_assert(TC_NPROD <= STAGES, "producer round-robin needs TC_NPROD <= STAGES");
+    static_assert(NPROD <= STAGES, "producer round-robin needs NPROD <= STAGES");
     const int pidx = warp == TC_PROD_WARP ? 0 : warp - 1;
     const bool leader = elect_one();
     const CUtensorMap* amap = &dp->amap;
@@ -255,7 +296,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int n0 = (unit0 % nt) * bn + static_cast<int>(rank) * (bn / CG);
       int tr = 0, ts = 0, cb = 0;
       for (int kb = 0; kb < npre; ++kb) {
-        if (kb % TC_NPROD == pidx) {
+        if (kb % NPROD == pidx) {
           if (rank == 0) mbar_arrive_expect_tx(&full[kb], a_tx1 + b_tx1);
           uint8_t* dst = sB + kb * C::B_BYTES;
           if (CG == 2)
@@ -287,7 +328,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int w0 = ow * p.stride - pad, h0 = oh * p.stride - pad;
       int cb = kb_lo % cblocks, ts = (kb_lo / cblocks) % ka, tr = kb_lo / cblocks / ka;
       for (int kb = kb_lo; kb < kb_hi; kb += KPS, ++g) {
-        if (g % TC_NPROD != pidx) {  // another producer's block: advance the (tap, channel) walk
+        if (g % NPROD != pidx) {  // another producer's block: advance the (tap, channel) walk
 #pragma unroll
           for (int j = 0; j < KPS; ++j) {
             if (++cb == cblocks) {
@@ -418,7 +459,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           in.sh[q] = d.shift ? __ldg(d.shift + (EPI == 2 ? min(col + q, d.cout - 1) : col + q)) : 0.f;
       }
       }
-      if (p.res && !(p.dbg & 2048)) {
+      if (RESB != 2 && p.res && !(p.dbg & 2048)) {
 #pragma unroll
         for (int r4 = 0; r4 < 4; ++r4) {
           const int m = m0 + rsub + 8 * r4;
@@ -451,6 +492,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int i = stripe ? 0 : group;  // tile ordinal
     int t = unit0 + i * ustep;
     int c = c0;
+    int rk = 0;  // RESB = 2: chunks this group has drained (residual ring sequence)
     EpiIn cur;  // this chunk's SubnetNorm row + residual (no register prefetch:
                 // 12 warps hide the latency, and 512 threads cap registers at 128)
     while (t < units) {
@@ -506,6 +548,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_tempty(a);
+      }
+      if (RESB == 2 && has_res) {  // this chunk's residual rows from the group's ring slot
+        const int slot = group * 2 + (rk & 1);
+        mbar_wait(&rfull[slot], static_cast<uint32_t>(rk >> 1) & 1);
+        const uint8_t* rs = sR + slot * TC_RR_SLOT + (quarter * 32 + rsub) * 64 + seg * 16;
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) cur.rv[r4] = *reinterpret_cast<const uint4*>(rs + r4 * 8 * 64);
+        // generic-proxy reads ordered before the producer's next async-proxy (TMA) write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[slot]);
+        ++rk;
       }
       const long long tsec = prof ? clock64() : 0;
       if (colok && !(p.dbg & 1)) {
@@ -795,6 +849,22 @@ int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, in
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
 }
 
+// Residual source of a conv: [rows][cout] bf16 with {32 columns, 128 rows}
+// boxes, no swizzle (64-byte rows: the epilogue's 16-byte row-segment reads
+// of 8 lanes cover two whole rows, conflict-free).
+int make_res_map(CUtensorMap* map, const void* r, long rows, int cout) {
+  static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
+  if (!enc || (cout & 7) != 0) return -1;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cout), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cout) * 2};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(TC_BM)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(r), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS ? 0 : -static_cast<int>(res);
+}
+
 // A operand: im2col map over a compact NHWC bf16 activation [n][h][w][cin]
 // for a k x k / stride / pad convolution: 128 pixels x 64 channels per load.
 int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
@@ -894,7 +964,7 @@ int choose_bn(int cout_max, long M, int nk_max) {
 // instances trade ring stages for the 96 KB weight block.
 #define SSN_TC_INSTANCES(X) X(64, 7, 1, 0, 1) X(128, 5, 1, 0, 1) X(256, 3, 1, 0, 1) \
   X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2) X(128, 7, 1, 0, 2) \
-  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2)
+  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2) X(256, 2, 1, 2, 1)
 
 cudaError_t init_conv_tc() {
 #define SSN_TC_ATTR(BN, ST, KPS, RB, CG)                                                  \
@@ -1016,6 +1086,10 @@ cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap,
     if (p.cg2) return launch_impl<192, 6, 1, 0, 2>(p, wmap, s);
     return launch_impl<192, 4, 1, 0>(p, wmap, s);
   }
+  if (resb && p.res && p.rres && !(dbg & 2097152) &&
+      static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK) * p.bn * TC_BK * 2 <=
+          TC_RB2_BYTES)
+    return launch_impl<256, 2, 1, 2>(p, wmap, s);  // residual through the TMA ring
   if (resb) return launch_impl<256, 4, 1, 1>(p, wmap, s);
   // bn > 128: pair tiles (cta_group::2) unless SSN_TC_DEBUG & 16384
   if (p.cg2) return launch_impl<256, 5, 1, 0, 2>(p, wmap, s);

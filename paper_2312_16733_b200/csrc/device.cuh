@@ -25,6 +25,10 @@ struct alignas(64) OpDesc {
   const float* scale;  // SubnetNorm folded scale [cout] (NULL = 1)
   const float* shift;  // SubnetNorm folded shift / bias [cout] (NULL = 0)
   int aux;             // OP_SE: active squeeze width
+  // residual source of a bf16 tcgen05 conv as THIS subnet lays it out:
+  // 2-D tiled map over [rows][cout_a], box {32 columns, 128 rows} (conv_tc
+  // RESB = 2 streams it through a shared-memory ring)
+  CUtensorMap rmap;
 };
 
 // GELU / tanh are out of line: inlined into the unrolled GEMM epilogues their
@@ -121,6 +125,7 @@ struct ConvParams {
   // `ws` ([splits][M][cout_a]); conv_finish_kernel adds them + the epilogue
   int splits;
   float* ws;
+  int rres;           // the descriptor row carries rmap for this op (engine)
   int dbg;            // profiling knob (SSN_TC_DEBUG): 1 = epilogue skips global
                       // memory, 2 = no MMA issued (bottleneck isolation only)
 };

@@ -36,6 +36,7 @@ int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, 
 int choose_bn(int cout_max, long M, int nk_max);
 bool conv_tc_use_pairs(const ConvParams& p);
 int conv_tc_splits(const ConvParams& p);
+int make_res_map(CUtensorMap* map, const void* r, long rows, int cout);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t init_conv_halo();
@@ -361,6 +362,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       } else if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M, o.k_max * o.k_max * ((t.cin_store + 63) / 64));
         p.ws = e->d_ws;
+        p.rres = p.res != nullptr && (o.cout_max & 7) == 0;  // every subnet's row carries rmap
         p.splits = conv_tc_splits(p);
         p.cg2 = p.splits > 1 ? 0 : conv_tc_use_pairs(p);
         CUtensorMap wmap{};
@@ -581,13 +583,17 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
   // physical input buffer of every op this subnet runs; a segment whose
   // blocks are all skipped (LayerSelect) leaves its input where it is.
   std::vector<const void*> in_ptr(st.plan.ops.size(), nullptr);
+  std::vector<const void*> res_ptr(st.plan.ops.size(), nullptr);
   bool flip = false;
   for (size_t si = 0; si < nseg; ++si) {
     st.seg_var[si] = st.seg_mask[si] | (flip ? SEG_FLIP : 0u);
     const auto sp = segment_plan(e, static_cast<int>(si), st.seg_var[si]);
     st.seg_run[si] = !sp.empty();
     if (sp.empty()) flip = !flip;
-    for (const SlotMap& sm : sp) in_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in, sm.map);
+    for (const SlotMap& sm : sp) {
+      in_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in, sm.map);
+      res_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].res, sm.map);
+    }
   }
   std::vector<OpDesc> row(st.plan.ops.size());
   for (size_t oi = 0; oi < st.plan.ops.size(); ++oi) {
@@ -602,9 +608,15 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
         if (make_halo_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
                               o.win, o.cin, o.k) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (halo) failed for op " + std::to_string(oi));
-      } else if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                              o.win, o.cin, o.k, o.stride, o.k / 2) != 0) {
-        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed for op " + std::to_string(oi));
+      } else {
+        if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
+                         o.win, o.cin, o.k, o.stride, o.k / 2) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed for op " + std::to_string(oi));
+        // residual source for conv_tc's TMA residual ring
+        if (res_ptr[oi] && (o.cout & 7) == 0 &&
+            make_res_map(&dsc.rmap, res_ptr[oi],
+                         static_cast<long>(e->desc.max_batch) * o.hout * o.wout, o.cout) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (residual) failed for op " + std::to_string(oi));
       }
     }
     dsc.cin = o.cin;
