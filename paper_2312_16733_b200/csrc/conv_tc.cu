@@ -82,9 +82,12 @@ template <int BN_MAX, int STAGES, int KPS, int RESB = 0, int CG = 1>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN_MAX / CG * TC_BK * 2;  // CG = 2: this CTA's half of N
-  static constexpr int RB = RESB == 2 ? TC_RB2_BYTES : (RESB ? TC_RB_BYTES : 0);
-  static constexpr int RR = RESB == 2 ? TC_RR_SLOT * TC_RR_SLOTS : 0;
-  static constexpr int STAGE_BYTES = KPS * (A_BYTES + (RESB ? 0 : B_BYTES));
+  // RESB: 0 streamed B, 1 resident B (96 KB), 2 resident B (64 KB) + residual
+  // ring, 3 streamed B + residual ring
+  static constexpr bool RES_B = RESB == 1 || RESB == 2;
+  static constexpr int RB = RESB == 2 ? TC_RB2_BYTES : (RESB == 1 ? TC_RB_BYTES : 0);
+  static constexpr int RR = RESB >= 2 ? TC_RR_SLOT * TC_RR_SLOTS : 0;
+  static constexpr int STAGE_BYTES = KPS * (A_BYTES + (RES_B ? 0 : B_BYTES));
   // TMEM accumulator ring: as many BN_MAX-column buffers as fit 512 columns
   // (max 4), so the MMA can run several tiles ahead of the epilogue.
   // (BN_MAX 64 -> 3: narrow tiles alternate whole across the 3 epilogue
@@ -142,6 +145,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
   using C = TcCfg<BN_MAX, STAGES, KPS, RESB, CG>;
   static_assert(CG == 1 || (RESB == 0 && KPS == 1), "2-CTA mode streams both operands");
+  constexpr bool RES_B = C::RES_B;         // resident weight slice
+  constexpr bool RRING = RESB >= 2;        // residual through the TMA ring
   constexpr int NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned for SW128; offset arithmetic on smem_raw keeps the shared
@@ -229,12 +234,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   long long w_wait = 0, w_wait2 = 0;
   const long long t_begin = prof ? clock64() : 0;
 
-  constexpr int NPROD = RESB == 2 ? 2 : TC_NPROD;  // RESB = 2: warp 3 streams the residual
-  if (RESB == 2 && warp == TC_PROD3_WARP) {
+  constexpr int NPROD = RRING ? 2 : TC_NPROD;  // residual ring: warp 3 streams the residual
+  if (RRING && warp == TC_PROD3_WARP) {
     // ============================================================ residual ring
     // Chunk c of every tile goes to group c % 3's ring (the group drains
     // its chunks in this same order), slot = that group's sequence % 2.
-    static_assert(RESB != 2 || CG == 1, "residual ring: single-CTA tiles");
+    static_assert(!RRING || CG == 1, "residual ring: single-CTA tiles");
     pdl_wait();  // the residual is the predecessors' output
     const bool leader = elect_one();
     const int nchunk = (bn + 31) / 32;
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const CUtensorMap* amap = &dp->amap;
     const int hwo = p.ho * p.wo;
     const bool pointwise = p.k_max == 1 && p.stride == 1;  // A map is 2-D tiled (make_act_map)
-    if (RESB && leader && pidx == 0) {
+    if (RES_B && leader && pidx == 0) {
       // the whole (single-N-tile) weight slice, once per CTA: block kb = (tap, channel block)
       if (p.dbg & 8) {
         mbar_arrive(bfull);
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // B of the first tile's leading ring stages, ahead of the PDL wait
-    const int npre = (KPS == 1 && !RESB && !(p.dbg & 8) && S == 1) ? min(STAGES, nk) : 0;
+    const int npre = (KPS == 1 && !RES_B && !(p.dbg & 8) && S == 1) ? min(STAGES, nk) : 0;
     const uint32_t a_tx1 = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
     const uint32_t b_tx1 = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
     if (npre && leader) {
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (leader && rank == 0 && !pre) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
           const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
-          const uint32_t tx = nsub * (a_tx + (RESB ? 0u : b_tx));
+          const uint32_t tx = nsub * (a_tx + (RES_B ? 0u : b_tx));
           if (tx) mbar_arrive_expect_tx(&full[s], tx);
           else mbar_arrive(&full[s]);
         }
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                               static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
               }
             }
-            if (leader && !RESB && !(p.dbg & 8) && !pre) {
+            if (leader && !RES_B && !(p.dbg & 8) && !pre) {
               uint8_t* dst = sB + (s * KPS + j) * C::B_BYTES;
               if (CG == 2)
                 tma2_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           in.sh[q] = d.shift ? __ldg(d.shift + (EPI == 2 ? min(col + q, d.cout - 1) : col + q)) : 0.f;
       }
       }
-      if (RESB != 2 && p.res && !(p.dbg & 2048)) {
+      if (!RRING && p.res && !(p.dbg & 2048)) {
 #pragma unroll
         for (int r4 = 0; r4 < 4; ++r4) {
           const int m = m0 + rsub + 8 * r4;
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (lane == 0) arrive_tempty(a);
       }
-      if (RESB == 2 && has_res) {  // this chunk's residual rows from the group's ring slot
+      if (RRING && has_res) {  // this chunk's residual rows from the group's ring slot
         const int slot = group * 2 + (rk & 1);
         mbar_wait(&rfull[slot], static_cast<uint32_t>(rk >> 1) & 1);
         const uint8_t* rs = sR + slot * TC_RR_SLOT + (quarter * 32 + rsub) * 64 + seg * 16;
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t idesc = umma_idesc_bf16(bn, TC_BM * CG);
     const uint64_t a_base = umma_desc_sw128(smem_u32(sA));
     const uint64_t b_base = umma_desc_sw128(smem_u32(sB));
-    if (RESB) {
+    if (RES_B) {
       mbar_wait(bfull, 0);
       tc_fence_after();
     }
@@ -709,7 +714,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (j < nsub) {
             const uint64_t ad = a_base + static_cast<uint64_t>(((s * KPS + j) * C::A_BYTES) >> 4);
             const uint64_t bd =
-                b_base + static_cast<uint64_t>(((RESB ? kb + j : s * KPS + j) * C::B_BYTES) >> 4);
+                b_base + static_cast<uint64_t>(((RES_B ? kb + j : s * KPS + j) * C::B_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 16; ++kk) {
               if (p.dbg & 2) continue;
@@ -964,7 +969,7 @@ int choose_bn(int cout_max, long M, int nk_max) {
 // instances trade ring stages for the 96 KB weight block.
 #define SSN_TC_INSTANCES(X) X(64, 7, 1, 0, 1) X(128, 5, 1, 0, 1) X(256, 3, 1, 0, 1) \
   X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2) X(128, 7, 1, 0, 2) \
-  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2) X(256, 2, 1, 2, 1)
+  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2) X(256, 2, 1, 2, 1) X(192, 3, 1, 3, 1)
 
 cudaError_t init_conv_tc() {
 #define SSN_TC_ATTR(BN, ST, KPS, RB, CG)                                                  \
@@ -1084,6 +1089,8 @@ cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap,
   }
   if (p.bn <= 192 && !resb && !(dbg & 524288)) {  // 144..192-wide tiles: deeper rings than BN 256
     if (p.cg2) return launch_impl<192, 6, 1, 0, 2>(p, wmap, s);
+    if (p.res && p.rres && p.splits <= 1 && !(dbg & 4194304))
+      return launch_impl<192, 3, 1, 3>(p, wmap, s);  // streamed B + residual ring
     return launch_impl<192, 4, 1, 0>(p, wmap, s);
   }
   if (resb && p.res && p.rres && !(dbg & 2097152) &&
