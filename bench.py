@@ -177,7 +177,6 @@ def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
     import paper_2312_16733_b200 as ssn
-    import torch.distributed as dist
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -210,16 +209,7 @@ def run_ours(args, rank, world, local_rank):
             k += eng.stats()["last_forward_kernels"]
         return k
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    from paper_2312_16733_b200.replicas import barrier, max_over_ranks
 
     # ---- device-resident timed region
     for i in range(args.warmup):
