@@ -248,6 +248,8 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
               rv[j] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.res) +
                                                            rowoff + c * 32 + 8 * j));
         }
+        uint4 pk_lo = make_uint4(0u, 0u, 0u, 0u);
+        bool paired = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int col = c * 32 + 8 * j;
@@ -301,7 +303,21 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
           pk.y = pack_bf16x2(o[2], o[3]);
           pk.z = pack_bf16x2(o[4], o[5]);
           pk.w = pack_bf16x2(o[6], o[7]);
-          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + rowoff + col) = pk;
+          __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + rowoff + col;
+          // row-per-lane stores: pair two 8-column groups into one 32-byte
+          // (full-sector) store where the row segment is 32-byte aligned
+          if ((j & 1) == 0 && col + 16 <= d.cout && ((rowoff + col) & 15) == 0) {
+            pk_lo = pk;
+            paired = true;
+          } else if ((j & 1) == 1 && paired) {
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(yp - 8),
+                         "r"(pk_lo.x), "r"(pk_lo.y), "r"(pk_lo.z), "r"(pk_lo.w), "r"(pk.x), "r"(pk.y),
+                         "r"(pk.z), "r"(pk.w)
+                         : "memory");
+            paired = false;
+          } else {
+            *reinterpret_cast<uint4*>(yp) = pk;
+          }
         }
       }
     }
