@@ -46,6 +46,7 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (64, 7, 7, 720, 720, 2048, 2048, 1, 1, 0),       # 31: stage-4 expand
     (64, 14, 14, 1024, 1024, 360, 360, 1, 1, 0),     # 32: stage-3 reduce
     (64, 112, 112, 32, 32, 64, 64, 3, 1, 0),         # 33: max stem 3x3 32->64 (halo)
+    (64, 112, 112, 32, 32, 32, 32, 3, 1, 1),         # 34: stem residual block (halo + residual)
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
