@@ -361,6 +361,10 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
         CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
       } else if (bf && !o.depthwise) {
         p.bn = choose_bn(o.cout_max, p.M, o.k_max * o.k_max * ((t.cin_store + 63) / 64));
+        // classifier head at <= 128 rows: one M tile, so the N width sets the
+        // CTA count — 64-wide tiles put 16 SMs (not 4) on the 32 K blocks
+        if (o.kind == OP_LINEAR && p.M <= 128 && o.cout_max > 64 && !(tc_debug_flags() & 262144))
+          p.bn = 64;
         p.ws = e->d_ws;
         p.rres = p.res != nullptr && (o.cout_max & 7) == 0;  // every subnet's row carries rmap
         p.splits = conv_tc_splits(p);
