@@ -2,6 +2,7 @@
 // SubNetAct kernels (tcgen05 / TMEM / TMA / mbarrier / cp.async).
 #pragma once
 
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -585,9 +586,12 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int n = 0;
-  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[n].val.programmaticStreamSerializationAllowed = 1;
-  ++n;
+  static const bool no_pdl = getenv("SSN_NO_PDL") != nullptr;  // debugging: plain stream order
+  if (!no_pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
   if (cluster_x > 1) {
     at[n].id = cudaLaunchAttributeClusterDimension;
     at[n].val.clusterDim.x = cluster_x;
