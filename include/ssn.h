@@ -189,6 +189,10 @@ int ssn_query(ssn_engine* eng, ssn_stats* out);
 /* Device pointer of the engine's last output logits (float32). */
 int ssn_device_logits(ssn_engine* eng, const float** out);
 
+/* Debugging: run subnet `id` op by op (no graphs) on the last staged input
+ * and store an FNV-1a hash of every op's output in sums[op] (0 = not run). */
+int ssn_debug_op_checksums(ssn_engine* eng, uint32_t id, uint32_t batch, uint64_t* sums,
+                           uint32_t n_ops);
 const char* ssn_last_error(void);
 
 /* ---- operator-level entry points (the paper's operators on raw device

@@ -151,6 +151,7 @@ def lib() -> ctypes.CDLL:
         "ssn_synchronize": (i32, [P, P]),
         "ssn_profile_latency": (i32, [P, u32, u32, u32, ctypes.POINTER(ctypes.c_double)]),
         "ssn_profile_ops": (i32, [P, u32, u32, u32, P, u32]),
+        "ssn_debug_op_checksums": (i32, [P, u32, u32, P, u32]),
         "ssn_query": (i32, [P, ctypes.POINTER(Stats)]),
         "ssn_device_logits": (i32, [P, ctypes.POINTER(P)]),
         "ssn_last_error": (ctypes.c_char_p, []),
@@ -308,6 +309,15 @@ class Engine:
         out = np.zeros(512, dtype=np.float32)
         check(lib().ssn_profile_ops(self._h, subnet_id, batch, iters, out.ctypes.data, 512),
               "profile_ops")
+        return out
+
+    def debug_op_checksums(self, subnet_id: int, batch: int):
+        """Debugging: per-op FNV-1a hash of every op's output (op-by-op run
+        on the last staged input; 0 = op not run)."""
+        import numpy as np
+        out = np.zeros(512, dtype=np.uint64)
+        check(lib().ssn_debug_op_checksums(self._h, subnet_id, batch, out.ctypes.data, 512),
+              "debug_op_checksums")
         return out
 
     def stats(self) -> dict:

@@ -193,6 +193,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
   const int cblocks = (d.cin + TC_BK - 1) / TC_BK;
   const int nk = ka * ka * cblocks;
+  // resident B: K blocks packed at the ACTUAL tile width (bn rows of 128 B,
+  // a multiple of the 1 KB swizzle atom), which is what resident_b() sizes
+  // against TC_RB_BYTES — a BN_MAX stride overran the region for bn < BN_MAX
+  const uint32_t rb_stride = static_cast<uint32_t>(bn) * TC_BK * 2;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nk * bn * TC_BK * 2));
         int tr = 0, ts = 0, cb = 0;
         for (int kb = 0; kb < nk; ++kb) {
-          tma_load_3d(sB + kb * C::B_BYTES, &wmap, bfull, cb * TC_BK,
+          tma_load_3d(sB + kb * rb_stride, &wmap, bfull, cb * TC_BK,
                       (tr + koff) * p.k_max + (ts + koff), 0);
           if (++cb == cblocks) {
             cb = 0;
@@ -714,7 +718,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (j < nsub) {
             const uint64_t ad = a_base + static_cast<uint64_t>(((s * KPS + j) * C::A_BYTES) >> 4);
             const uint64_t bd =
-                b_base + static_cast<uint64_t>(((RES_B ? kb + j : s * KPS + j) * C::B_BYTES) >> 4);
+                b_base + static_cast<uint64_t>(
+                             (RES_B ? (kb + j) * rb_stride : (s * KPS + j) * C::B_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 16; ++kk) {
               if (p.dbg & 2) continue;

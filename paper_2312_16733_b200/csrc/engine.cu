@@ -1033,6 +1033,37 @@ int ssn_profile_ops(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t iters, 
   });
 }
 
+int ssn_debug_op_checksums(ssn_engine* e, uint32_t id, uint32_t batch, uint64_t* sums,
+                           uint32_t n_ops) {
+  return guarded([&] {
+    if (!e || !sums) SSN_THROW(SSN_E_INVALID, "bad arguments");
+    if (n_ops < e->net.ops.size()) SSN_THROW(SSN_E_RANGE, "sums too small");
+    if (batch == 0 || batch > e->desc.max_batch) SSN_THROW(SSN_E_RANGE, "batch out of range");
+    if (ssn_actuate(e, id) != SSN_OK) SSN_THROW(SSN_E_RANGE, g_last_error);
+    const SubnetState& sub = e->subs[id];
+    cudaStream_t s = e->stream;
+    CUDA_TRY(launch_set_row(e->d_rowptr, sub.d_row, s));
+    e->dirty = false;
+    for (uint32_t i = 0; i < n_ops; ++i) sums[i] = 0;
+    std::vector<uint8_t> host;
+    for (size_t si = 0; si < e->net.segments.size(); ++si)
+      for (const SlotMap& sm : segment_plan(e, static_cast<int>(si), sub.seg_var[si])) {
+        const int k = enqueue_op(e, sm.op, sm.map, batch, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (k == 0) continue;
+        const OpSpec& o = e->net.ops[sm.op];
+        const OpSpec& a = sub.plan.ops[sm.op];
+        const size_t elem = o.kind == OP_LINEAR ? 4 : (e->bf16 ? 2 : 4);
+        const size_t bytes = static_cast<size_t>(batch) * o.hout * o.wout * a.cout * elem;
+        host.resize(bytes);
+        CUDA_TRY(cudaMemcpy(host.data(), slot_ptr(e, o.out, sm.map), bytes, cudaMemcpyDeviceToHost));
+        uint64_t h = 1469598103934665603ull;  // FNV-1a over the op's output bytes
+        for (uint8_t b : host) h = (h ^ b) * 1099511628211ull;
+        sums[sm.op] = h;
+      }
+  });
+}
+
 int ssn_query(ssn_engine* e, ssn_stats* out) {
   return guarded([&] {
     if (!e || !out) SSN_THROW(SSN_E_INVALID, "null argument");

@@ -105,6 +105,19 @@ def test_conv_bf16_residual_and_f32_out(gpu):
     assert np.abs(got - ref).max() / np.abs(ref).max() < 5e-3
 
 
+@pytest.mark.parametrize("cin", [192, 208, 256])
+def test_conv_bf16_resident_slice_narrower_than_instance(gpu, cin):
+    """Resident-B 1x1 with bn (176) < the instance's BN_MAX (256), four K
+    blocks and several tiles per CTA: the resident slice is packed at the
+    actual tile width.  (A BN_MAX block stride once overran the 96 KB region
+    into the epilogue's staging tile — wrong, run-to-run varying results.)
+    Checked against the oracle for several active widths."""
+    for cout in (104, 176):
+        got, ref = _run_bf16(gpu, 32, 28, 28, cin, 256, cout, 176, 1, 1, act=1)  # 196 tiles
+        err = np.abs(got - ref).max() / (np.abs(ref).max() + 1e-6)
+        assert err < 1e-2, (cin, cout, err)
+
+
 @pytest.mark.parametrize("cout", [2, 10, 13])
 def test_conv_bf16_ragged_cout(gpu, cout):
     """cout % 8 != 0 (e.g. a 2-label classifier) takes the scalar epilogue tail."""
