@@ -268,6 +268,7 @@ def run_ours(args, rank, world, local_rank):
     act = measure_actuation(eng, torch, stream, xs[0], B)
 
     roof = live_roofline(eng, desc, cfgs, B, peaks, ssn)
+    parity = None if args.no_parity else parity_check(eng, cfgs, xs[0], B, stream, torch)
     families = None if args.no_families else family_rows(ssn, peaks, local_rank)
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -293,11 +294,42 @@ def run_ours(args, rank, world, local_rank):
         "per_subnet": per_subnet,
         "families": families,
         "cpu_baseline": cpu,
+        "parity": parity,
         "engine": {k: v for k, v in eng.stats().items()
                    if k in ("weight_bytes", "norm_table_bytes", "arena_bytes", "graphs_built")},
     }
     eng.close()
     print(json.dumps(line), flush=True)
+
+
+def parity_check(eng, cfgs, x, B, stream, torch):
+    """CHECKER, outside every timed region: image 0 of the bench's own input
+    batch, run on the bench's own bs-B graph of each sweep subnet (default
+    SubnetNorm rows, the ids the timed steps use), against the CPU oracle
+    (bf16 activation storage emulated, and pure fp32).  The oracle is never
+    the thing measured."""
+    import numpy as np
+    from oracle import oracle as O
+    on = O.OracleNet(2, seed=0, classes=1000, bf16_weights=True)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-12))  # noqa: E731
+    xs = ((x[:1].cpu().numpy().astype(np.float32) - 128.0) / 64.0).transpose(0, 3, 1, 2).copy()
+    out = {}
+    for sid, name in enumerate(SUBNETS):
+        logits = np.zeros((B, 1000), np.float32)
+        eng.actuate(sid)
+        eng.forward(x, B, B, logits, stream=stream.cuda_stream)
+        stream.synchronize()
+        got = logits[0]
+        emu = on.forward(cfgs[sid], xs, subnet_id=sid, bf16_storage=True)[0]
+        ref = on.forward(cfgs[sid], xs, subnet_id=sid)[0]
+        out[name] = {"rel_vs_bf16_storage_oracle": round(rel(got, emu), 5),
+                     "rel_vs_fp32_oracle": round(rel(got, ref), 5),
+                     "all_rows_finite": bool(np.isfinite(logits).all()),
+                     "argmax_equal": bool(got.argmax() == emu.argmax())}
+    out["tolerance"] = f"rel L2 <= 2e-2 (bf16); image 0 of the timed batch on the bs{B} graph"
+    out["pass"] = all(v["all_rows_finite"] and v["rel_vs_bf16_storage_oracle"] <= 2e-2 and
+                      v["rel_vs_fp32_oracle"] <= 2e-2 for k, v in out.items() if k in SUBNETS)
+    return out
 
 
 def measure_actuation(eng, torch, stream, x, B):
@@ -451,6 +483,7 @@ def main():
     ap.add_argument("--no-families", action="store_true",
                     help="skip the OFA-MBv3 / BERT rows (configs 3 and 5)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity field")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

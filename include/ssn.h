@@ -43,8 +43,8 @@ extern "C" {
 enum ssn_family {
   SSN_FAMILY_TINYCNN = 1,       /* BASELINE config 1      */
   SSN_FAMILY_OFA_RESNET50 = 2,  /* BASELINE config 2      */
-  SSN_FAMILY_OFA_MBV3 = 3,      /* BASELINE config 3 (reserved, next row)  */
-  SSN_FAMILY_BERT = 4           /* BASELINE config 5 (reserved, next row)  */
+  SSN_FAMILY_OFA_MBV3 = 3,      /* BASELINE config 3      */
+  SSN_FAMILY_BERT = 4           /* BASELINE config 5      */
 };
 
 enum ssn_dtype { SSN_DTYPE_F32 = 0, SSN_DTYPE_BF16 = 1 };
@@ -150,10 +150,18 @@ int ssn_subnet_stat_count(ssn_engine* eng, const ssn_subnet_cfg* cfg,
 
 /* Register subnet `id` (the index into the pareto-sorted catalog, reference
  * policy.hpp:187-190) with its control tuple and SubnetNorm statistics.
- * bn_mean / bn_var == NULL -> deterministic defaults from ssn_rng.h.
+ * bn_mean / bn_var == NULL -> deterministic defaults from ssn_rng.h; else both
+ * must hold exactly ssn_subnet_stat_count(cfg) floats (the C-ABI cannot check
+ * the length: use ssn_register_subnet_n, which takes it).
  * Folds (gamma, beta, mu_{i,j}, var_{i,j}) into per-channel scale/shift. */
 int ssn_register_subnet(ssn_engine* eng, uint32_t id, const ssn_subnet_cfg* cfg,
                         const float* bn_mean, const float* bn_var);
+
+/* Same, with the length of bn_mean / bn_var: fails with SSN_E_INVALID unless
+ * n_stats == ssn_subnet_stat_count(cfg) (or both arrays are NULL), and when
+ * exactly one of the two arrays is NULL. */
+int ssn_register_subnet_n(ssn_engine* eng, uint32_t id, const ssn_subnet_cfg* cfg,
+                          const float* bn_mean, const float* bn_var, uint64_t n_stats);
 
 /* Build the LayerSelect CUDA-graph segments for every batch in the grid
  * (the catalog's profiled batch sizes, reference profile.hpp:164-171). */
@@ -166,7 +174,11 @@ int ssn_actuate(ssn_engine* eng, uint32_t id);
  * (reference ClampedDispatch, policy.hpp:219-232).  `x` and `logits` may be
  * host or device pointers; logits are float32 [count][num_classes].
  * Enqueued on `stream` (cudaStream_t, NULL = engine stream); returns after
- * enqueue — call ssn_synchronize() before reading host logits. */
+ * enqueue — call ssn_synchronize() before reading host logits.
+ * Forwards of one engine share its arena, staged input and active-subnet
+ * word: a forward enqueued on a different stream than the engine's previous
+ * call is ordered after that call (an engine-owned event), so streams may be
+ * mixed but forwards of one engine never overlap on the device. */
 int ssn_forward(ssn_engine* eng, const void* x, uint32_t count,
                 uint32_t profiled_batch, float* logits, void* stream);
 

@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "ssn.h"
@@ -30,6 +32,14 @@ inline void check(int rc) {
   }
 }
 
+// servesim::SubnetConfig has no kernel list (profile.hpp:28-54); a config type
+// that carries one (`kernel_sizes`, OFA-MBv3) passes it through.
+template <class T, class = void>
+struct has_kernel_sizes : std::false_type {};
+template <class T>
+struct has_kernel_sizes<T, std::void_t<decltype(std::declval<const T&>().kernel_sizes)>>
+    : std::true_type {};
+
 // Owning view of a control tuple in C-ABI form.
 struct CfgView {
   std::vector<uint8_t> d;
@@ -41,12 +51,16 @@ struct CfgView {
     for (bool f : cfg.depth_flags) d.push_back(f ? 1 : 0);
     e.assign(cfg.expand_ratios.begin(), cfg.expand_ratios.end());
     w.assign(cfg.width_multipliers.begin(), cfg.width_multipliers.end());
+    if constexpr (has_kernel_sizes<Cfg>::value)  // elastic-kernel supernets (OFA-MBv3)
+      for (auto ks : cfg.kernel_sizes) k.push_back(static_cast<uint32_t>(ks));
     c.depth_flags = d.data();
     c.n_depth = static_cast<uint32_t>(d.size());
     c.expand_ratios = e.data();
     c.n_expand = static_cast<uint32_t>(e.size());
     c.width_multipliers = w.data();
     c.n_width = static_cast<uint32_t>(w.size());
+    c.kernel_sizes = k.empty() ? nullptr : k.data();
+    c.n_kernel = static_cast<uint32_t>(k.size());
   }
 };
 

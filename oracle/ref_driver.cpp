@@ -1,9 +1,10 @@
 // ref_driver.cpp — TEST INFRASTRUCTURE. A thin CLI over the UNMODIFIED
 // reference scheduling path (servesim headers under /root/reference, compiled
 // by oracle/Makefile into oracle/_ref/servesim_ref).  It is the
-// subnet-selection oracle: the engine's C++ SlackFit mirror
-// (paper_2312_16733_b200/csrc/slackfit.hpp) must reproduce its decisions and
-// dispatch logs bit-exactly.  No reference source is copied into this repo.
+// subnet-selection oracle: the engine keeps the reference's SlackFit as its
+// caller (no mirror of it exists here), and the tests pin that caller's
+// decisions and dispatch logs to the frozen values of the reference's own
+// tests.  No reference source is copied into this repo.
 //
 //   servesim_ref decide   <catalog.csv|default> <bucket_count> <slack_us>...
 //       one line per slack: "<slack> <batch> <subnet_index> <latency_us>"

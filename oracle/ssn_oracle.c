@@ -849,10 +849,23 @@ static void bert_forward(Ctx* c, const ssn_subnet_cfg* s, const int* ids, int n,
             sum += sc[j];
           }
           float* out = ctx + ((size_t)b * S + i) * Ca + h * 64;
-          for (int j = 0; j < S; ++j) {
-            const float pj = (float)(sc[j] / sum);
-            const float* vj = V + ((size_t)b * S + j) * Ca + h * 64;
-            for (int e = 0; e < 64; ++e) out[e] += pj * vj[e];
+          if (c->emulate_bf16) {
+            /* engine storage: the UNNORMALISED probabilities exp(s - max) are
+             * the bf16 A operand of the P.V product; the row sum (fp32, from
+             * the unrounded values) divides the fp32 accumulator afterwards */
+            for (int j = 0; j < S; ++j) {
+              const float pj = ssn_round_bf16(sc[j]);
+              const float* vj = V + ((size_t)b * S + j) * Ca + h * 64;
+              for (int e = 0; e < 64; ++e) out[e] += pj * vj[e];
+            }
+            const float inv = (float)(1.0 / sum);
+            for (int e = 0; e < 64; ++e) out[e] *= inv;
+          } else {
+            for (int j = 0; j < S; ++j) {
+              const float pj = (float)(sc[j] / sum);
+              const float* vj = V + ((size_t)b * S + j) * Ca + h * 64;
+              for (int e = 0; e < 64; ++e) out[e] += pj * vj[e];
+            }
           }
         }
         free(sc);

@@ -145,6 +145,7 @@ def lib() -> ctypes.CDLL:
         "ssn_destroy": (None, [P]),
         "ssn_subnet_stat_count": (i32, [P, cfg_p, ctypes.POINTER(u64)]),
         "ssn_register_subnet": (i32, [P, u32, cfg_p, fp, fp]),
+        "ssn_register_subnet_n": (i32, [P, u32, cfg_p, fp, fp, u64]),
         "ssn_prepare": (i32, [P, ctypes.POINTER(u32), u32]),
         "ssn_actuate": (i32, [P, u32]),
         "ssn_forward": (i32, [P, P, u32, u32, P, P]),
@@ -266,12 +267,19 @@ class Engine:
         s, keep = cfg_to_c(cfg)
         fp = ctypes.POINTER(ctypes.c_float)
         m = v = None
+        n = 0
+        if (bn_mean is None) != (bn_var is None):
+            raise ValueError("SubnetNorm statistics need both bn_mean and bn_var (or neither)")
         if bn_mean is not None:
             bn_mean = np.ascontiguousarray(bn_mean, dtype=np.float32)
             bn_var = np.ascontiguousarray(bn_var, dtype=np.float32)
+            if bn_mean.ndim != 1 or bn_var.shape != bn_mean.shape:
+                raise ValueError("bn_mean / bn_var must be 1-D arrays of equal length")
+            n = bn_mean.size
             m = bn_mean.ctypes.data_as(fp)
             v = bn_var.ctypes.data_as(fp)
-        check(lib().ssn_register_subnet(self._h, subnet_id, ctypes.byref(s), m, v),
+        # the length-checked entry point: a short array is an error, never a heap over-read
+        check(lib().ssn_register_subnet_n(self._h, subnet_id, ctypes.byref(s), m, v, n),
               f"register_subnet({subnet_id})")
 
     def prepare(self, batch_grid: Sequence[int]):

@@ -1,14 +1,17 @@
 """In-tree build of the SubNetAct engine (libssn.so) for sm_100a.
 
 Explicit nvcc (no JIT cache): the .so lands next to this file so it travels
-to the GPU box with the repo snapshot.
+to the GPU box with the repo snapshot.  Each translation unit compiles to its
+own object in parallel (build/), then one nvcc link makes the shared library.
 """
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
 OUT = os.path.join(HERE, "libssn.so")
 SOURCES = ["engine.cu", "conv_tc.cu", "conv_halo.cu", "kernels.cu", "transformer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -17,8 +20,8 @@ FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
     "--expt-relaxed-constexpr",
-    "-shared",
 ]
+LINK = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared"]
 
 
 def needs_build():
@@ -33,7 +36,19 @@ def needs_build():
 def build(force=False, verbose=True):
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", OUT + ".tmp"]
+    os.makedirs(OBJ, exist_ok=True)
+
+    def cc(src):
+        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(cc, SOURCES))
+    cmd = [NVCC] + LINK + objs + ["-o", OUT + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -585,7 +585,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           o[r4][4] = hi.x; o[r4][5] = hi.y; o[r4][6] = hi.z; o[r4][7] = hi.w;
         }
         if (S > 1) {  // split-K partial: raw fp32 into this K range's workspace slice
-          float* wz = p.ws + static_cast<size_t>(t - tt * S) * p.M * d.cout;
+          const int z = t - tt * S;
+          if (z * nk / S == (z + 1) * nk / S) {  // empty K range (nk < splits): zero slice
+#pragma unroll
+            for (int r4 = 0; r4 < 4; ++r4)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[r4][q] = 0.f;
+          }
+          float* wz = p.ws + static_cast<size_t>(z) * p.M * d.cout;
 #pragma unroll
           for (int r4 = 0; r4 < 4; ++r4) {
             const int m = m0 + rsub + 8 * r4;
@@ -701,6 +708,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_after();
       const uint32_t acc = tmem + a * BN_MAX;
+      if (kb_lo == kb_hi) {  // split-K range with no K block (nk < splits): publish
+        tc_commit_elect(&tfull[a]);  // the accumulator at once; the epilogue writes zeros
+        __syncwarp();
+        continue;
+      }
       for (int kb = kb_lo; kb < kb_hi; kb += KPS, ++g) {
         const int s = g % STAGES;
         const uint32_t ph = (g / STAGES) & 1;

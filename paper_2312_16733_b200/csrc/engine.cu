@@ -155,10 +155,26 @@ struct ssn_engine {
   std::map<uint64_t, std::pair<cudaGraphExec_t, int>> graphs;  // key -> (exec, kernels)
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // Cross-stream ordering: forwards share engine state (the active-row word,
+  // the arena, d_raw, d_logits, the staging slots), so a call enqueued on a
+  // different stream than the previous one first waits for that one's work.
+  cudaEvent_t last_done = nullptr;
+  cudaStream_t last_stream = nullptr;
   double last_actuate_us = 0, last_forward_host_us = 0;
   uint32_t last_kernels = 0, last_graphs = 0;
   bool prepared = false;
 };
+
+// Order `s` after the engine's previous call when that call used another stream.
+static void order_stream(ssn_engine* e, cudaStream_t s) {
+  if (e->last_stream != nullptr && e->last_stream != s)
+    CUDA_TRY(cudaStreamWaitEvent(s, e->last_done, 0));
+}
+
+static void mark_done(ssn_engine* e, cudaStream_t s) {
+  CUDA_TRY(cudaEventRecord(e->last_done, s));
+  e->last_stream = s;
+}
 
 static uint64_t graph_key(int seg, uint32_t mask, uint32_t batch) {
   return (static_cast<uint64_t>(seg) << 48) | (static_cast<uint64_t>(mask) << 32) | batch;
@@ -795,6 +811,7 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     CUDA_TRY(cudaMemset(e->d_rowptr, 0, sizeof(OpDesc*)));
     CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&e->last_done, cudaEventDisableTiming));
     *out = e.release();
   });
 }
@@ -823,6 +840,7 @@ void ssn_destroy(ssn_engine* e) {
   cudaFree(e->d_w);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  if (e->last_done) cudaEventDestroy(e->last_done);
   delete e;
 }
 
@@ -838,6 +856,24 @@ int ssn_register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c, con
                         const float* var) {
   return guarded([&] {
     if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    register_subnet(e, id, c, mean, var);
+  });
+}
+
+int ssn_register_subnet_n(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c, const float* mean,
+                          const float* var, uint64_t n_stats) {
+  return guarded([&] {
+    if (!e || !c) SSN_THROW(SSN_E_INVALID, "null argument");
+    if ((mean == nullptr) != (var == nullptr))
+      SSN_THROW(SSN_E_INVALID, "SubnetNorm statistics need both mean and var (or neither)");
+    if (mean) {
+      SubnetCfg cfg = SubnetCfg::from_c(c);
+      const uint64_t need = build_net(e->desc, &cfg).stat_count;
+      if (n_stats != need)
+        SSN_THROW(SSN_E_INVALID, "SubnetNorm statistics length " + std::to_string(n_stats) +
+                                     " != stat count " + std::to_string(need));
+    }
     CUDA_TRY(cudaSetDevice(e->device));
     register_subnet(e, id, c, mean, var);
   });
@@ -906,6 +942,7 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
     const SubnetState& sub = e->subs[e->active];
     uint32_t kernels = 0, graphs = 0;
+    order_stream(e, s);
     if (e->dirty) {
       CUDA_TRY(launch_set_row(e->d_rowptr, sub.d_row, s));
       e->dirty = false;
@@ -944,6 +981,7 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
       CUDA_TRY(cudaMemcpyAsync(logits, e->d_logits,
                                static_cast<size_t>(count) * e->desc.num_classes * 4,
                                cudaMemcpyDefault, s));
+    mark_done(e, s);
     e->last_kernels = kernels;
     e->last_graphs = graphs;
   });
@@ -998,6 +1036,7 @@ int ssn_profile_ops(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t iters, 
     if (ssn_actuate(e, id) != SSN_OK) SSN_THROW(SSN_E_RANGE, g_last_error);
     const SubnetState& sub = e->subs[id];
     cudaStream_t s = e->stream;
+    order_stream(e, s);
     CUDA_TRY(launch_set_row(e->d_rowptr, sub.d_row, s));
     e->dirty = false;
     const size_t nop = e->net.ops.size();
@@ -1030,6 +1069,7 @@ int ssn_profile_ops(ssn_engine* e, uint32_t id, uint32_t batch, uint32_t iters, 
       std::sort(v.begin(), v.end());
       op_us[op] = v[v.size() / 2];
     }
+    mark_done(e, s);
   });
 }
 
@@ -1042,6 +1082,7 @@ int ssn_debug_op_checksums(ssn_engine* e, uint32_t id, uint32_t batch, uint64_t*
     if (ssn_actuate(e, id) != SSN_OK) SSN_THROW(SSN_E_RANGE, g_last_error);
     const SubnetState& sub = e->subs[id];
     cudaStream_t s = e->stream;
+    order_stream(e, s);
     CUDA_TRY(launch_set_row(e->d_rowptr, sub.d_row, s));
     e->dirty = false;
     for (uint32_t i = 0; i < n_ops; ++i) sums[i] = 0;
@@ -1061,6 +1102,7 @@ int ssn_debug_op_checksums(ssn_engine* e, uint32_t id, uint32_t batch, uint64_t*
         for (uint8_t b : host) h = (h ^ b) * 1099511628211ull;
         sums[sm.op] = h;
       }
+    mark_done(e, s);
   });
 }
 
@@ -1107,13 +1149,20 @@ static OpDesc plain_desc(int cin, int cout, int k, int pad, const float* scale,
   return d;
 }
 
+// Device copy of an operator-API OpDesc: a 64-slot ring PER DEVICE (keyed by
+// the current device, so a second GPU never dereferences the first one's
+// memory).  The upload is synchronous on the caller's stream; a slot is
+// rewritten 64 calls later, so callers spreading operator calls over several
+// streams must keep fewer than 64 of them in flight.
 static OpDesc* op_desc_scratch(const OpDesc& d, cudaStream_t s) {
-  static OpDesc* dev = nullptr;
+  static std::map<int, std::pair<OpDesc*, unsigned>> ring;  // device -> (slots, next)
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
-  if (!dev) CUDA_TRY(cudaMalloc(&dev, sizeof(OpDesc) * 64));
-  static int slot = 0;
-  OpDesc* p = dev + (slot++ % 64);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  auto& r = ring[dev];
+  if (!r.first) CUDA_TRY(cudaMalloc(&r.first, sizeof(OpDesc) * 64));
+  OpDesc* p = r.first + (r.second++ % 64);
   CUDA_TRY(cudaMemcpyAsync(p, &d, sizeof(OpDesc), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return p;
