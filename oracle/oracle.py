@@ -119,13 +119,18 @@ class OracleNet:
             raise ValueError(lib().oracle_last_error().decode())
         return out
 
-    def forward_tokens(self, cfg, ids, bf16_storage=False):
+    def forward_tokens(self, cfg, ids, bf16_storage=False, acc64=False):
+        """BERT logits; acc64 accumulates the linears in double (a second,
+        equally valid implementation of the same bf16-storage semantics: the
+        spread between the two measures how implementation-sensitive the
+        bf16-stored network is on these inputs)."""
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         n, seq = ids.shape
         out = np.zeros((n, self.classes), dtype=np.float32)
         s, keep = _cfg(cfg)
-        rc = lib().oracle_forward_tokens(self.h, ctypes.byref(s), _p(ids), n, seq,
-                                         1 if bf16_storage else 0, _p(out))
+        flags = (1 if bf16_storage else 0) | (4 if acc64 else 0)
+        rc = lib().oracle_forward_tokens(self.h, ctypes.byref(s), _p(ids), n, seq, flags,
+                                         _p(out))
         if rc:
             raise ValueError(lib().oracle_last_error().decode())
         return out

@@ -157,6 +157,8 @@ typedef struct {
   size_t stat_cursor;  /* floats consumed / produced                       */
   int active_norms;
   int count_only;      /* only count statistics                            */
+  int acc64;           /* BERT linears accumulate in double (sensitivity
+                          probe of the bf16-storage emulation, flag bit 2) */
 } Ctx;
 
 static void store_round(Ctx* c, T4* t) {
@@ -762,7 +764,8 @@ static int bert_check(const ssn_subnet_cfg* s) {
 }
 
 /* y[t][:cout] = x[t][:cin] . W[:cout][:cin]^T + b[:cout] (+ act), rows x cols */
-static float* linear_(const float* x, int rows, int cin, const OTensor* T, int cout, int act) {
+static float* linear_(const float* x, int rows, int cin, const OTensor* T, int cout, int act,
+                      int acc64) {
   float* y = (float*)malloc(sizeof(float) * (size_t)rows * cout);
 #pragma omp parallel for schedule(static)
   for (int r = 0; r < rows; ++r)
@@ -770,8 +773,14 @@ static float* linear_(const float* x, int rows, int cin, const OTensor* T, int c
       const float* wp = T->w + (size_t)co * T->cin;
       const float* xp = x + (size_t)r * cin;
       float acc = 0.f;
+      if (acc64) {
+        double a = 0.0;
+        for (int i = 0; i < cin; ++i) a += (double)xp[i] * wp[i];
+        acc = (float)a;
+      } else {
 #pragma omp simd reduction(+ : acc)
-      for (int i = 0; i < cin; ++i) acc += xp[i] * wp[i];
+        for (int i = 0; i < cin; ++i) acc += xp[i] * wp[i];
+      }
       float v = acc + T->bias[co];
       if (act == 3) v = 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
       if (act == 4) v = tanhf(v);
@@ -822,9 +831,9 @@ static void bert_forward(Ctx* c, const ssn_subnet_cfg* s, const int* ids, int n,
   for (int l = 0; l < BT_L; ++l) {
     if (!s->depth_flags[l]) continue; /* LayerSelect */
     const int tb = 3 + 6 * l;
-    float* Q = linear_(X, T, BT_HID, &o->t[tb], Ca, 0);
-    float* K = linear_(X, T, BT_HID, &o->t[tb + 1], Ca, 0);
-    float* V = linear_(X, T, BT_HID, &o->t[tb + 2], Ca, 0);
+    float* Q = linear_(X, T, BT_HID, &o->t[tb], Ca, 0, c->acc64);
+    float* K = linear_(X, T, BT_HID, &o->t[tb + 1], Ca, 0, c->acc64);
+    float* V = linear_(X, T, BT_HID, &o->t[tb + 2], Ca, 0, c->acc64);
     round_buf(c, Q, (size_t)T * Ca);
     round_buf(c, K, (size_t)T * Ca);
     round_buf(c, V, (size_t)T * Ca);
@@ -871,14 +880,14 @@ static void bert_forward(Ctx* c, const ssn_subnet_cfg* s, const int* ids, int n,
         free(sc);
       }
     round_buf(c, ctx, (size_t)T * Ca);
-    float* O = linear_(ctx, T, Ca, &o->t[tb + 3], BT_HID, 0);
+    float* O = linear_(ctx, T, Ca, &o->t[tb + 3], BT_HID, 0, c->acc64);
     for (size_t i = 0; i < (size_t)T * BT_HID; ++i) O[i] += X[i];
     round_buf(c, O, (size_t)T * BT_HID);
     layernorm_(O, T, &o->nm[1 + 2 * l]);
     round_buf(c, O, (size_t)T * BT_HID);
-    float* F = linear_(O, T, BT_HID, &o->t[tb + 4], ffn, 3);
+    float* F = linear_(O, T, BT_HID, &o->t[tb + 4], ffn, 3, c->acc64);
     round_buf(c, F, (size_t)T * ffn);
-    float* Y = linear_(F, T, ffn, &o->t[tb + 5], BT_HID, 0);
+    float* Y = linear_(F, T, ffn, &o->t[tb + 5], BT_HID, 0, c->acc64);
     for (size_t i = 0; i < (size_t)T * BT_HID; ++i) Y[i] += O[i];
     round_buf(c, Y, (size_t)T * BT_HID);
     layernorm_(Y, T, &o->nm[2 + 2 * l]);
@@ -889,9 +898,9 @@ static void bert_forward(Ctx* c, const ssn_subnet_cfg* s, const int* ids, int n,
   float* cls = (float*)malloc(sizeof(float) * (size_t)n * BT_HID);
   for (int b = 0; b < n; ++b)
     memcpy(cls + (size_t)b * BT_HID, X + (size_t)b * S * BT_HID, sizeof(float) * BT_HID);
-  float* P = linear_(cls, n, BT_HID, &o->t[3 + 6 * BT_L], BT_HID, 4);
+  float* P = linear_(cls, n, BT_HID, &o->t[3 + 6 * BT_L], BT_HID, 4, c->acc64);
   round_buf(c, P, (size_t)n * BT_HID);
-  float* L = linear_(P, n, BT_HID, &o->t[4 + 6 * BT_L], o->classes, 0);
+  float* L = linear_(P, n, BT_HID, &o->t[4 + 6 * BT_L], o->classes, 0, c->acc64);
   memcpy(logits, L, sizeof(float) * (size_t)n * o->classes);
   free(cls); free(P); free(L); free(X);
 }
@@ -1077,6 +1086,7 @@ int oracle_forward_tokens(oracle_net* o, const ssn_subnet_cfg* s, const int* ids
   memset(&c, 0, sizeof c);
   c.o = o;
   c.emulate_bf16 = flags & 1;
+  c.acc64 = (flags >> 2) & 1;
   bert_forward(&c, s, ids, n, seq, logits);
   return 0;
 }

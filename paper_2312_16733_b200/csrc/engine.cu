@@ -939,6 +939,7 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
       SSN_THROW(SSN_E_INVALID, "count must be in [1, profiled_batch]");
     if (std::find(e->grid.begin(), e->grid.end(), profiled_batch) == e->grid.end())
       SSN_THROW(SSN_E_RANGE, "batch size " + std::to_string(profiled_batch) + " not prepared");
+    CUDA_TRY(cudaSetDevice(e->device));  // the calling worker thread may not have it current
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
     const SubnetState& sub = e->subs[e->active];
     uint32_t kernels = 0, graphs = 0;
@@ -994,6 +995,7 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
 int ssn_synchronize(ssn_engine* e, void* stream) {
   return guarded([&] {
     if (!e) SSN_THROW(SSN_E_INVALID, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
     CUDA_TRY(cudaStreamSynchronize(stream ? static_cast<cudaStream_t>(stream) : e->stream));
   });
 }

@@ -15,6 +15,7 @@ import pytest
 
 import paper_2312_16733_b200 as ssn
 from oracle import oracle as O
+from parity import check_bert
 
 pytestmark = pytest.mark.gpu
 
@@ -40,9 +41,7 @@ def test_bert_ffn_expand_0p1_small_batch(gpu):
             for b in (1, 2):
                 ids = O.tokens(SEED, 20 + b, b, 128)
                 got = eng.infer(ids, b, b)
-                emu = on.forward_tokens(c, ids, bf16_storage=True)
-                assert np.isfinite(got).all()
-                assert rel(got, emu) <= 2e-2, (i, b, rel(got, emu))
+                check_bert(f"bert ffn-narrow {i} bs{b}", got, on, c, ids)
 
 
 R50_NARROW = {
