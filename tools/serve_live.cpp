@@ -20,6 +20,8 @@
 //   actuation the reference simulator with the MEASURED actuation cost vs the
 //             100 ms model-switching baseline (simcore.hpp:247-252,
 //             acceptance.cpp:271-285).                                (§8f-4)
+//   simulate  the reference router's SlackFit dispatch log for N replicas
+//             (servesim::run), replayed per rank by bench.py.      (config 4)
 //
 // Every mode prints one JSON object.  Payloads: `Query` carries no image
 // (edf_queue.hpp:16-31); a batch's images are a contiguous slice of a
@@ -522,6 +524,45 @@ int cmd_actuation(const std::map<std::string, std::string>& a) {
   return 0;
 }
 
+// ---------------------------------------------------------------- simulate
+// The reference router's decisions for a bursty trace on `workers` replicas
+// (servesim::run, simcore.hpp:129, with its DispatchLog): one TSV row per
+// dispatch "worker subnet_index actual_count profiled_batch start_us
+// predicted_us", for bench.py's multi-replica SlackFit replay.  No engine.
+int cmd_simulate(const std::map<std::string, std::string>& a) {
+  const servesim::Catalog cat = servesim::pareto_filter(
+      servesim::load_catalog(arg(a, "catalog", "catalog_b200.csv")));
+  const uint32_t workers = std::stoul(arg(a, "workers", "1"));
+  const double load = std::stod(arg(a, "load", "0.3"));
+  const double cap0 = servesim::sustainable_qps(cat, cat.at(0).id, 1);
+  servesim::TraceSpec spec;
+  spec.kind = servesim::TraceKind::Bursty;
+  spec.base_rate = 0.2 * load * workers * cap0;
+  spec.variant_rate = 0.8 * load * workers * cap0;
+  spec.cv2 = std::stod(arg(a, "cv2", "4"));
+  spec.duration_s = std::stod(arg(a, "duration", "1"));
+  spec.slo_us = static_cast<Micros>(std::stod(arg(a, "slo-factor", "3")) * cat.at(cat.size() - 1).max_latency());
+  spec.seed = std::stoull(arg(a, "seed", "7"));
+  const servesim::Trace trace = servesim::generate_trace(spec);
+  servesim::SimConfig sc;
+  sc.worker_count = workers;
+  sc.actuation_delay_us = std::stoull(arg(a, "actuation-us", "1"));
+  sc.policy = servesim::PolicyKind::slackfit();
+  servesim::DispatchLog log;
+  const servesim::SimReport rep = servesim::run(trace, cat, sc, &log);
+  std::ofstream out(arg(a, "log", "dispatch.tsv"));
+  for (const auto& r : log)
+    out << r.worker << '\t' << r.subnet_index << '\t' << r.actual_count << '\t' << r.profiled_batch
+        << '\t' << r.start_us << '\t' << r.predicted_latency_us << '\n';
+  json j = servesim::report_to_json(rep);
+  j["mode"] = "simulate";
+  j["dispatches"] = log.size();
+  j["lambda_qps"] = load * workers * cap0;
+  j["sub0_capacity_qps"] = cap0;
+  std::cout << j.dump() << std::endl;
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) try {
@@ -535,6 +576,7 @@ int main(int argc, char** argv) try {
   if (cmd == "serve") return cmd_serve(a);
   if (cmd == "memory") return cmd_memory(a);
   if (cmd == "actuation") return cmd_actuation(a);
+  if (cmd == "simulate") return cmd_simulate(a);
   std::cerr << "unknown mode " << cmd << "\n";
   return 2;
 } catch (const std::exception& e) {
