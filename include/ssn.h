@@ -223,6 +223,18 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin,
                      const float* shift, const void* res, int act, int out_f32,
                      void* y, void* stream);
 
+/* Depthwise WeightSlice conv (OFA elastic kernel) + SubnetNorm + activation,
+ * bf16 (the OFA-MBv3 dw layers of ssn_forward run this kernel):
+ * x: [n][h][w][c] bf16 compact (c % 8 == 0); y: [n][ho][wo][c] bf16
+ * wgt: bf16 tap-major [k_max][k_max][c_max]; the active k x k kernel is the
+ *      centre crop, the active channels the leading c (read in place)
+ * pad = k / 2; scale/shift float32 [c] (NULL -> 1 / 0)
+ * act: 0 none, 1 relu, 2 h_swish.  k in {3, 5, 7} <= k_max <= 7, stride 1/2.
+ * Replaces the per-request worker sleep for these layers (serve_runtime.hpp:167). */
+int ssn_op_dw_bf16(const void* x, int n, int h, int w, int c, const void* wgt,
+                   int c_max, int k_max, int k, int stride, const float* scale,
+                   const float* shift, int act, void* y, void* stream);
+
 /* Same operator, float32 SIMT path (config-1 parity precision). groups ==
  * cin means depthwise with weights [c_max][k_max][k_max] centre-cropped to k. */
 int ssn_op_conv_f32(const float* x, int n, int h, int w, int cin,

@@ -1071,6 +1071,7 @@ int oracle_conv_op(const float* x, int n, int h, int w, int cin, const float* wg
       v = v * (scale ? scale[co] : 1.f) + (shift ? shift[co] : 0.f);
       if (res) v += res[(size_t)p * cout + co];
       if (act == 1) v = v > 0.f ? v : 0.f;
+      else if (act == 2) v = v * fminf(fmaxf(v + 3.f, 0.f), 6.f) / 6.f;  /* h_swish (line 271) */
       y[(size_t)p * cout + co] = v;
     }
   }

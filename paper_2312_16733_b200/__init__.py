@@ -158,6 +158,7 @@ def lib() -> ctypes.CDLL:
         "ssn_last_error": (ctypes.c_char_p, []),
         "ssn_op_conv_bf16": (i32, [P, i32, i32, i32, i32, P, i32, i32, i32, i32, i32, i32,
                                    P, P, P, i32, i32, P, P]),
+        "ssn_op_dw_bf16": (i32, [P, i32, i32, i32, i32, P, i32, i32, i32, i32, P, P, i32, P, P]),
         "ssn_op_conv_f32": (i32, [P, i32, i32, i32, i32, P, i32, i32, i32, i32, i32, i32, i32,
                                   i32, P, P, P, i32, P, P]),
     }
@@ -344,6 +345,14 @@ def op_conv_bf16(x, n, h, w, cin, wgt, cout_max, cin_max, k, stride, pad, cout, 
     check(lib().ssn_op_conv_bf16(_ptr(x), n, h, w, cin, _ptr(wgt), cout_max, cin_max, k, stride,
                                  pad, cout, _ptr(scale), _ptr(shift), _ptr(res), act, out_f32,
                                  _ptr(y), _ptr(stream)), "op_conv_bf16")
+
+
+def op_dw_bf16(x, n, h, w, c, wgt, c_max, k_max, k, stride, scale=None, shift=None, act=0,
+               y=None, stream=None):
+    """Depthwise bf16 operator (weights tap-major [k_max][k_max][c_max])."""
+    check(lib().ssn_op_dw_bf16(_ptr(x), n, h, w, c, _ptr(wgt), c_max, k_max, k, stride,
+                               _ptr(scale), _ptr(shift), act, _ptr(y), _ptr(stream)),
+          "op_dw_bf16")
 
 
 def op_conv_f32(x, n, h, w, cin, wgt, cout_max, cin_max, k_max, k, stride, pad, cout,

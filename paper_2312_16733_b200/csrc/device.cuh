@@ -98,6 +98,10 @@ struct SEParams {
   int op;
   int n, hw, c_max, se_max;
   int w_ld;  // row stride of the reduce tensor (this op's max channels)
+  // > 0: the producing depthwise kernel already summed the activation per
+  // tile into parts_buf [n][parts][c_max]; the pool pass only adds the parts
+  int parts;
+  const float* parts_buf;
 };
 
 // Static (graph-baked) parameters of one conv op.
@@ -129,6 +133,11 @@ struct ConvParams {
   int rres;           // the descriptor row carries rmap for this op (engine)
   int dbg;            // profiling knob (SSN_TC_DEBUG): 1 = epilogue skips global
                       // memory, 2 = no MMA issued (bottleneck isolation only)
+  // depthwise (dw.cu): TMA stage ring, and the fused squeeze-excite pool:
+  // per-tile channel sums of the stored activation -> pool[n][tile][pool_ld]
+  int dw_stages, dw_stage_bytes;
+  float* pool;
+  int pool_ld;
 };
 
 

@@ -49,6 +49,10 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
 cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s);
+int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int k,
+                    int stride, int wo);
+int dw_tiles_per_image(int stride, int ho, int wo);
+bool dw_supported(int k_max, int k, int stride);
 cudaError_t launch_se(const SEParams& p, cudaStream_t s);
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s);
 cudaError_t launch_layernorm(const LnParams& p, cudaStream_t s);
@@ -150,6 +154,7 @@ struct ssn_engine {
   int stage_slot = 0;
   float* d_logits = nullptr;
   float* d_se = nullptr;  // squeeze-excite scratch: pooled + gate [max_batch][se_cmax]
+  float* d_separt = nullptr;  // SE pool partials of the depthwise kernel [max_batch][tiles][se_cmax]
   int se_cmax = 0;
   std::vector<uint32_t> grid;
   std::map<uint64_t, std::pair<cudaGraphExec_t, int>> graphs;  // key -> (exec, kernels)
@@ -286,6 +291,18 @@ static bool stem_fused(const ssn_engine* e, int ci) {
          !(tc_debug_flags() & 65536);
 }
 
+// bf16 depthwise op `di` whose output feeds a squeeze-excite op: the
+// depthwise kernel sums the activation per tile (fused SE pool); returns the
+// partial count per image, 0 = not fused.
+static int se_fused_parts(const ssn_engine* e, int di) {
+  if (!e->bf16 || di < 0 || di + 1 >= static_cast<int>(e->net.ops.size())) return 0;
+  const OpSpec& d = e->net.ops[di];
+  const OpSpec& se = e->net.ops[di + 1];
+  if (d.kind != OP_CONV || !d.depthwise || se.kind != OP_SE || se.in != d.out) return 0;
+  if (tc_debug_flags() & 1048576) return 0;  // A/B switch: unfused SE pool
+  return dw_tiles_per_image(d.stride, d.hout, d.wout);
+}
+
 static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cudaStream_t s) {
   const OpSpec& o = e->net.ops[oi];
   const bool bf = e->bf16;
@@ -392,6 +409,10 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
         CUDA_TRY(launch_conv_tc(p, wmap, s));
         return p.splits > 1 ? 2 : 1;  // + conv_finish_kernel
       } else if (bf) {
+        if (se_fused_parts(e, oi) > 0) {
+          p.pool = e->d_separt;
+          p.pool_ld = e->se_cmax;
+        }
         CUDA_TRY(launch_dw_bf16(p, s));
       } else {
         CUDA_TRY(launch_conv_f32(p, s));
@@ -464,6 +485,8 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.c_max = e->se_cmax;
       p.se_max = o.se_mid_max;
       p.w_ld = o.cin_max;
+      p.parts = se_fused_parts(e, oi - 1);
+      p.parts_buf = e->d_separt;
       CUDA_TRY(launch_se(p, s));
       return 4;
     }
@@ -620,6 +643,12 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     const OpSpec& o = st.plan.ops[oi];
     OpDesc& dsc = row[oi];
     std::memset(&dsc, 0, sizeof(dsc));
+    if (e->bf16 && o.active && o.kind == OP_CONV && o.depthwise) {
+      // depthwise input window map (box sized for this subnet's k)
+      if (make_dw_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
+                          o.win, o.cout, o.k, o.stride, o.wout) != 0)
+        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (depthwise) failed for op " + std::to_string(oi));
+    }
     if (e->bf16 && o.active && (o.kind == OP_CONV || o.kind == OP_LINEAR) && !o.depthwise) {
       // WeightSlice A operand: im2col TMA map over this subnet's compact
       // activation (cin_a channels) in the buffer its graph variant reads.
@@ -807,6 +836,12 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     if (e->se_cmax)  // pooled [B][cmax] | gate [B][cmax] | hidden [B][hmax]
       CUDA_TRY(cudaMalloc(&e->d_se, 1ull * desc->max_batch * (2 * e->se_cmax + se_hmax) *
                                         sizeof(float)));
+    int se_parts = 0;
+    for (int oi = 0; oi < static_cast<int>(e->net.ops.size()); ++oi)
+      se_parts = std::max(se_parts, se_fused_parts(e.get(), oi));
+    if (se_parts)
+      CUDA_TRY(cudaMalloc(&e->d_separt,
+                          1ull * desc->max_batch * se_parts * e->se_cmax * sizeof(float)));
     CUDA_TRY(cudaMalloc(&e->d_rowptr, sizeof(OpDesc*)));
     CUDA_TRY(cudaMemset(e->d_rowptr, 0, sizeof(OpDesc*)));
     CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
@@ -836,6 +871,7 @@ void ssn_destroy(ssn_engine* e) {
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   cudaFree(e->d_logits);
   cudaFree(e->d_se);
+  cudaFree(e->d_separt);
   cudaFree(e->d_rowptr);
   cudaFree(e->d_w);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -1225,6 +1261,44 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.cg2 ? p.bn / 2 : p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
     CUDA_TRY(launch_conv_tc(p, wmap, s));
+  });
+}
+
+int ssn_op_dw_bf16(const void* x, int n, int h, int w, int c, const void* wgt, int c_max,
+                   int k_max, int k, int stride, const float* scale, const float* shift, int act,
+                   void* y, void* stream) {
+  return guarded([&] {
+    if (!x || !wgt || !y) SSN_THROW(SSN_E_INVALID, "null tensor");
+    if (n <= 0 || h <= 0 || w <= 0) SSN_THROW(SSN_E_INVALID, "bad geometry");
+    if (c <= 0 || c % 8 || c_max % 8 || c > c_max)
+      SSN_THROW(SSN_E_INVALID, "channels must be positive multiples of 8 within the max shape");
+    if (!dw_supported(k_max, k, stride) || k_max % 2 == 0)
+      SSN_THROW(SSN_E_INVALID, "depthwise k must be 3/5/7 <= k_max <= 7 (odd), stride 1 or 2");
+    if (act < 0 || act > 2) SSN_THROW(SSN_E_INVALID, "act must be 0 none, 1 relu, 2 h_swish");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int pad = k / 2;
+    const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
+    OpDesc d = plain_desc(c, c, k, pad, scale, shift);
+    if (make_dw_act_map(&d.amap, x, n, h, w, c, k, stride, wo) != 0)
+      SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (depthwise) failed");
+    ConvParams p{};
+    p.x = x;
+    p.y = y;
+    p.w = wgt;
+    p.fixed = op_desc_scratch(d, s);
+    p.n = n;
+    p.h = h;
+    p.w_ = w;
+    p.ho = ho;
+    p.wo = wo;
+    p.stride = stride;
+    p.M = n * ho * wo;
+    p.k_max = k_max;
+    p.cin_max = 1;
+    p.cout_max = c_max;
+    p.act = act;
+    p.depthwise = 1;
+    CUDA_TRY(launch_dw_bf16(p, s));
   });
 }
 

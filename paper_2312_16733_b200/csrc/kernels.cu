@@ -583,189 +583,6 @@ __global__ void conv_f32_kernel(ConvParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// bf16 depthwise k x k conv (OFA elastic kernel: centre crop of k_max = 7)
-// fused with SubnetNorm + activation; weights tap-major [k_max^2][c_max].
-//
-// Shared-memory tiled: a CTA owns an 8 x 8 output tile of 32 channels.  It
-// stages the input halo tile ((8-1)*S + k)^2 pixels x 64 B once with
-// coalesced 16-byte loads (zero fill at the image border / channel tail) and
-// the k x k x 32 weights, then each thread computes 4 adjacent outputs of 2
-// channels with packed fp32x2 FMAs (FFMA2) from shared memory.  Every input
-// byte leaves HBM once (halo re-reads hit L2: neighbouring tiles of a channel
-// chunk are adjacent in the launch order).  The previous per-thread register
-// scheme re-loaded each input element ~17x through L1 and ran at ~0.1 of the
-// HBM roofline on OFA-MBv3.
-// Bank layout: the two half-warps read rows S apart; the padded row stride
-// (== 64 mod 128 bytes per S rows) puts them in disjoint banks.
-
-constexpr int DWT_CC = 32;  // channels per CTA
-
-// Tile geometry per stride: TH x TW outputs, QW adjacent outputs per thread,
-// 16 channel pairs x (TH * TW / QW) threads = 256.
-template <int S>
-struct DwTile {
-  static constexpr int TH = S == 1 ? 16 : 8;
-  static constexpr int TW = 8;
-  static constexpr int QW = S == 1 ? 8 : 4;
-  static constexpr int IH = (TH - 1) * S + 7;  // staged rows/cols for k_max 7
-  static constexpr int IW = (TW - 1) * S + 7;
-  static constexpr int PIX = DWT_CC * 4;       // fp32 pixel: 128 B
-  static constexpr int IN_BYTES = IH * IW * PIX;
-  static constexpr int W_BYTES = 49 * PIX;
-  static constexpr int SMEM = IN_BYTES + W_BYTES;
-  static_assert(16 * TH * (TW / QW) == 256, "256 threads per tile");
-};
-
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long o;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(o)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
-        "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&o);
-}
-
-template <int S, int K>
-__device__ __forceinline__ void dw_tile_compute(const uint8_t* tile, const uint8_t* wts, int cp,
-                                                int orow, int ocol0,
-                                                float2 (&acc)[DwTile<S>::QW]) {
-  using T = DwTile<S>;
-  constexpr int SEG = (T::QW - 1) * S + K;
-#pragma unroll
-  for (int r = 0; r < K; ++r) {
-    const uint8_t* row = tile + ((orow * S + r) * T::IW + ocol0 * S) * T::PIX + cp * 8;
-    float2 in[SEG];
-#pragma unroll
-    for (int t = 0; t < SEG; ++t) in[t] = *reinterpret_cast<const float2*>(row + t * T::PIX);
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const float2 w = *reinterpret_cast<const float2*>(wts + (r * K + s) * T::PIX + cp * 8);
-#pragma unroll
-      for (int q = 0; q < T::QW; ++q) acc[q] = ffma2(in[q * S + s], w, acc[q]);
-    }
-  }
-}
-
-__device__ __forceinline__ void st_f32x8(uint8_t* dst, const uint4& v) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-  const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-  const float2 c = __bfloat1622float2(h[2]), e = __bfloat1622float2(h[3]);
-  reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
-  reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, e.x, e.y);
-}
-
-template <int S>
-__global__ void __launch_bounds__(256) dw_bf16_kernel(ConvParams p) {
-  pdl_wait();
-  pdl_trigger();
-  using T = DwTile<S>;
-  extern __shared__ __align__(16) uint8_t dsm[];
-  uint8_t* tile = dsm;                 // [IH][IW][32] fp32
-  uint8_t* wts = dsm + T::IN_BYTES;    // [k*k][32] fp32
-  const OpDims d = load_desc(p.row, p.fixed, p.op);
-  const int C = d.cout;
-  const int k = d.k, pad = d.pad, off = (p.k_max - k) / 2;
-  const int tw_n = (p.wo + T::TW - 1) / T::TW, th_n = (p.ho + T::TH - 1) / T::TH;
-  const int chunks = (p.cout_max + DWT_CC - 1) / DWT_CC;
-  // launch order (img, chunk, th, tw): spatial neighbours of one channel chunk
-  // run together, so halo re-reads are L2 hits
-  long b = blockIdx.x;
-  const int tw = static_cast<int>(b % tw_n);
-  b /= tw_n;
-  const int th = static_cast<int>(b % th_n);
-  b /= th_n;
-  const int cb = static_cast<int>(b % chunks);
-  const int img = static_cast<int>(b / chunks);
-  const int c0 = cb * DWT_CC;
-  if (c0 >= C) return;  // WeightSlice: chunks past the active width
-  const int oh0 = th * T::TH, ow0 = tw * T::TW;
-  const int ih0 = oh0 * S - pad, iw0 = ow0 * S - pad;
-  const int ih_a = (T::TH - 1) * S + k, iw_a = (T::TW - 1) * S + k;  // staged extent, active k
-  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x);
-  const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w);
-  const int tid = threadIdx.x;
-
-  // stage the input halo tile, converted to fp32 once.  Thread -> (16-byte
-  // quarter q of a pixel's 32 channels, column, row-in-block); all of its
-  // loads are issued before any conversion (memory-level parallelism), no
-  // integer division, and the two 16-byte halves of each fp32 quarter are
-  // written in pixel-parity order so a warp's stores hit all 8 bank groups.
-  {
-    constexpr int CP = S == 1 ? 16 : 32;  // columns per row block (>= IW)
-    constexpr int RP = 64 / CP;           // rows per block
-    constexpr int IT = (T::IH + RP - 1) / RP;
-    const int q = tid & 3, pl = tid >> 2;
-    const int col = pl & (CP - 1), rsub = pl / CP;
-    const int iw = iw0 + col;
-    const bool colok = col < iw_a && iw >= 0 && iw < p.w_ && c0 + q * 8 < C;
-    const __nv_bfloat16* xs = x + (static_cast<long>(img) * p.h * p.w_ + iw) * C + c0 + q * 8;
-    uint4 v[IT];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int r = it * RP + rsub;
-      const int ih = ih0 + r;
-      v[it] = make_uint4(0, 0, 0, 0);
-      if (colok && r < ih_a && ih >= 0 && ih < p.h)
-        v[it] = __ldg(reinterpret_cast<const uint4*>(xs + static_cast<long>(ih) * p.w_ * C));
-    }
-    const int h0 = (col & 1) * 16, h1 = 16 - h0;
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int r = it * RP + rsub;
-      if (r < ih_a && col < iw_a) {
-        uint8_t* dst = tile + (r * T::IW + col) * T::PIX + q * 32;
-        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[it]);
-        const float2 a = __bfloat1622float2(hv[0]), bq = __bfloat1622float2(hv[1]);
-        const float2 c = __bfloat1622float2(hv[2]), e = __bfloat1622float2(hv[3]);
-        const float4 lo = make_float4(a.x, a.y, bq.x, bq.y), hi = make_float4(c.x, c.y, e.x, e.y);
-        *reinterpret_cast<float4*>(dst + h0) = h0 ? hi : lo;
-        *reinterpret_cast<float4*>(dst + h1) = h0 ? lo : hi;
-      }
-    }
-  }
-  for (int idx = tid; idx < k * k * 4; idx += 256) {
-    const int q = idx & 3, tap = idx >> 2;
-    const int r = tap / k, s = tap - r * k;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (c0 + q * 8 < C)
-      v = __ldg(reinterpret_cast<const uint4*>(w + static_cast<long>((r + off) * p.k_max + s + off) *
-                                                       p.cout_max + c0 + q * 8));
-    st_f32x8(wts + tap * T::PIX + q * 32, v);
-  }
-  __syncthreads();
-
-  const int cp = tid & 15;  // channel pair
-  const int pg = tid >> 4;
-  const int orow = S == 1 ? pg : (pg & 7);
-  const int ocol0 = S == 1 ? 0 : (pg >> 3) * T::QW;
-  float2 acc[T::QW];
-#pragma unroll
-  for (int q = 0; q < T::QW; ++q) acc[q] = make_float2(0.f, 0.f);
-  if (k == 3)
-    dw_tile_compute<S, 3>(tile, wts, cp, orow, ocol0, acc);
-  else if (k == 5)
-    dw_tile_compute<S, 5>(tile, wts, cp, orow, ocol0, acc);
-  else
-    dw_tile_compute<S, 7>(tile, wts, cp, orow, ocol0, acc);
-
-  const int c = c0 + 2 * cp;
-  const int oh = oh0 + orow;
-  if (c >= C || oh >= p.ho) return;
-  const float2 sc = d.scale ? make_float2(d.scale[c], d.scale[c + 1]) : make_float2(1.f, 1.f);
-  const float2 sh = d.shift ? make_float2(d.shift[c], d.shift[c + 1]) : make_float2(0.f, 0.f);
-  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y) + (static_cast<long>(img * p.ho + oh) * p.wo) * C + c;
-#pragma unroll
-  for (int q = 0; q < T::QW; ++q) {
-    const int ow = ow0 + ocol0 + q;
-    if (ow >= p.wo) break;
-    const float2 v = ffma2(acc[q], sc, sh);
-    *reinterpret_cast<uint32_t*>(y + static_cast<long>(ow) * C) =
-        pack_bf16x2(act_apply(v.x, p.act), act_apply(v.y, p.act));
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Squeeze-excite (OFA DynamicSE): pool -> reduce FC + ReLU -> expand FC +
 // h_sigmoid -> scale the activation in place.
 
@@ -799,6 +616,22 @@ __global__ void se_pool_kernel(SEParams p) {
     for (int l = 0; l < 32; ++l) s += red[l][threadIdx.x];
     p.pooled[static_cast<long>(n) * p.c_max + c0 + threadIdx.x] = s / static_cast<float>(p.hw);
   }
+}
+
+// Fused-pool variant: the depthwise kernel left per-tile channel sums of its
+// stored output in parts_buf [n][parts][c_max]; add them in fixed order.
+// grid (n, ceil(c_max / 256)), one thread per channel.
+__global__ void __launch_bounds__(256) se_pool_parts_kernel(SEParams p) {
+  pdl_wait();
+  pdl_trigger();
+  const OpDesc* dp = desc_ptr(p.row, nullptr, p.op);
+  const int C = dp->cin;
+  const int n = blockIdx.x, c = blockIdx.y * 256 + threadIdx.x;
+  if (c >= C) return;
+  const float* src = p.parts_buf + static_cast<long>(n) * p.parts * p.c_max + c;
+  float s = 0.f;
+  for (int t = 0; t < p.parts; ++t) s += __ldg(src + static_cast<long>(t) * p.c_max);
+  p.pooled[static_cast<long>(n) * p.c_max + c] = s / static_cast<float>(p.hw);
 }
 
 // gate[n][c] = h_sigmoid(We[c, :mid] . relu(Wr[:mid, :C] . pooled[n] + br) + be[c]),
@@ -968,25 +801,11 @@ cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s) {
                     dim3(128), 0, s, 1, p);
 }
 
-template <int S>
-static cudaError_t launch_dw_tiles(const ConvParams& p, cudaStream_t s) {
-  using T = DwTile<S>;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      dw_bf16_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-  if (attr != cudaSuccess) return attr;
-  const long tiles = static_cast<long>(p.n) * ((p.ho + T::TH - 1) / T::TH) *
-                     ((p.wo + T::TW - 1) / T::TW) * ((p.cout_max + DWT_CC - 1) / DWT_CC);
-  return launch_pdl(dw_bf16_kernel<S>, dim3(static_cast<unsigned>(tiles)), dim3(256), T::SMEM, s,
-                    1, p);
-}
-
-cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s) {
-  if (p.k_max > 7 || (p.stride != 1 && p.stride != 2)) return cudaErrorInvalidValue;
-  return p.stride == 2 ? launch_dw_tiles<2>(p, s) : launch_dw_tiles<1>(p, s);
-}
-
 cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
-  cudaError_t e = launch_pdl(se_pool_kernel, dim3(p.n, (p.c_max + 63) / 64), dim3(256), 0, s, 1, p);
+  cudaError_t e =
+      p.parts > 0
+          ? launch_pdl(se_pool_parts_kernel, dim3(p.n, (p.c_max + 255) / 256), dim3(256), 0, s, 1, p)
+          : launch_pdl(se_pool_kernel, dim3(p.n, (p.c_max + 63) / 64), dim3(256), 0, s, 1, p);
   if (e != cudaSuccess) return e;
   const int nbk = (p.n + SE_NB - 1) / SE_NB;
   // one warp per output row

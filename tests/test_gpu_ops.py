@@ -159,3 +159,59 @@ def test_conv_f32_matches_oracle(gpu, depthwise):
     torch.cuda.synchronize()
     got = y.cpu().numpy()
     np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-4)
+
+
+# ---- depthwise bf16 (dw.cu: TMA-pipelined, elastic centre crop) ----------
+DW_CASES = [
+    # n, h, w, c, c_max, k_max, k, stride, act
+    (2, 14, 14, 64, 64, 7, 7, 1, 1),      # one chunk, full kernel
+    (2, 14, 14, 64, 64, 7, 3, 1, 2),      # centre crop 3 of 7, h_swish
+    (2, 28, 28, 144, 192, 7, 5, 1, 1),    # ragged chunk (144 = 2x64 + 16), 5 of 7
+    (3, 7, 7, 1152, 1152, 7, 7, 1, 2),    # 7 px tiles, many chunks
+    (2, 56, 56, 72, 144, 7, 3, 2, 1),     # stride 2, ragged 72
+    (2, 112, 112, 24, 24, 3, 3, 1, 1),    # c < 64 (box wider than the tensor)
+    (1, 13, 17, 40, 48, 5, 5, 2, 0),      # odd sizes, stride 2, no activation
+    (2, 9, 11, 32, 32, 7, 7, 1, 1),       # width not a multiple of 7, single chunk
+    (16, 14, 14, 816, 816, 7, 7, 2, 2),   # 14 -> 7 stride 2
+]
+
+
+def _run_dw(gpu, n, h, w, c, c_max, k_max, k, stride, act, seed=0):
+    import torch
+    rng = np.random.default_rng(seed)
+    pad = k // 2
+    x = rng.standard_normal((n, h, w, c)).astype(np.float32)
+    wmax = (rng.standard_normal((c_max, 1, k_max, k_max)) / k).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    shift = rng.uniform(-0.2, 0.2, c).astype(np.float32)
+    xb, wb = _bf16(x), _bf16(wmax)
+    ref = O.conv_op(xb.float().numpy(), wb.float().numpy(), c_max, c_max, k_max, k, stride, pad,
+                    c, depthwise=True, scale=scale, shift=shift, act=act)
+    wd = wb[:, 0].permute(1, 2, 0).contiguous().to(gpu)  # tap-major [k_max][k_max][c_max]
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    y = torch.full((n, ho, wo, c), float("nan"), dtype=torch.bfloat16, device=gpu)
+    ssn.op_dw_bf16(xb.to(gpu).contiguous(), n, h, w, c, wd, c_max, k_max, k, stride,
+                   torch.from_numpy(scale).to(gpu), torch.from_numpy(shift).to(gpu), act, y)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy(), ref
+
+
+@pytest.mark.parametrize("case", DW_CASES, ids=[str(c) for c in DW_CASES])
+def test_dw_bf16_matches_oracle(gpu, case):
+    got, ref = _run_dw(gpu, *case)
+    assert np.isfinite(got).all(), "unwritten outputs (NaN sentinel survived)"
+    scale = max(1.0, float(np.abs(ref).max()))
+    # fp32 accumulation of bf16 products, one bf16 rounding of the output
+    assert np.abs(got - ref).max() <= 1e-2 * scale
+
+
+def test_dw_bf16_rejects_bad_args(gpu):
+    import torch
+    x = torch.zeros(4096, device=gpu, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        ssn.op_dw_bf16(x, 1, 4, 4, 12, x, 16, 7, 3, 1, y=x)   # c % 8
+    with pytest.raises(ValueError):
+        ssn.op_dw_bf16(x, 1, 4, 4, 16, x, 16, 7, 9, 1, y=x)   # k > k_max
+    with pytest.raises(ValueError):
+        ssn.op_dw_bf16(x, 1, 4, 4, 16, x, 16, 7, 3, 3, y=x)   # stride 3
