@@ -168,7 +168,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
-  const int bn = p.bn;
+  // WeightSlice tile width of the actuated subnet (conv_bn_active); its own
+  // weight map (box = bn / CG rows) when the subnet row carries one that
+  // matches, else the graph's max-width map (extra rows land unused)
+  const int bn = (p.dbg & 4194304) ? p.bn : conv_bn_active(p.bn, d.cout, CG);  // A/B switch
+  const bool own_wmap = dp->wrows == bn / CG;
+  const CUtensorMap* wm = own_wmap ? &dp->wmap : &wmap;
+  const int brows = own_wmap ? bn / CG : p.bn / CG;  // rows each B box lands
   const int mt = (p.M + TC_BM * CG - 1) / (TC_BM * CG);  // CG = 2: 256-row pair tiles
   const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
   const int tiles = mt * nt;
@@ -181,7 +187,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // Epilogue work split: wide tiles (>= TC_EPI_GROUPS 32-column chunks) are
   // striped chunk-wise across all groups; narrow ones go whole to one group
   // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
-  const bool stripe = (bn + 31) / 32 >= TC_EPI_GROUPS;
+  // (a narrow ACTIVE width on a wide instance stripes too: the alternate mode
+  // needs NACC % 3 == 0, which only the 64-wide instances guarantee)
+  const bool stripe = (bn + 31) / 32 >= TC_EPI_GROUPS || C::NACC % TC_EPI_GROUPS != 0;
   // alternate mode hands tile i to group i % 3 and accumulator i % NACC: the
   // pair must be a function of the accumulator alone
   static_assert(BN_MAX > 64 || C::NACC % TC_EPI_GROUPS == 0, "accumulator/group mapping");
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // resident B: K blocks packed at the ACTUAL tile width (bn rows of 128 B,
   // a multiple of the 1 KB swizzle atom), which is what resident_b() sizes
   // against TC_RB_BYTES — a BN_MAX stride overran the region for bn < BN_MAX
-  const uint32_t rb_stride = static_cast<uint32_t>(bn) * TC_BK * 2;
+  const uint32_t rb_stride = static_cast<uint32_t>(brows) * TC_BK * 2;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&rempty[r], 4);  // the group's four warps
     }
     fence_mbar_init();
-    tma_prefetch(&wmap);
+    tma_prefetch(wm);
     tma_prefetch(&dp->amap);
   }
   if (warp == TC_MMA_WARP) {
@@ -282,10 +290,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (p.dbg & 8) {
         mbar_arrive(bfull);
       } else {
-        mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nk * bn * TC_BK * 2));
+        mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nk * brows * TC_BK * 2));
         int tr = 0, ts = 0, cb = 0;
         for (int kb = 0; kb < nk; ++kb) {
-          tma_load_3d(sB + kb * rb_stride, &wmap, bfull, cb * TC_BK,
+          tma_load_3d(sB + kb * rb_stride, wm, bfull, cb * TC_BK,
                       (tr + koff) * p.k_max + (ts + koff), 0);
           if (++cb == cblocks) {
             cb = 0;
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // B of the first tile's leading ring stages, ahead of the PDL wait
     const int npre = (KPS == 1 && !RES_B && !(p.dbg & 8) && S == 1) ? min(STAGES, nk) : 0;
     const uint32_t a_tx1 = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
-    const uint32_t b_tx1 = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
+    const uint32_t b_tx1 = (p.dbg & 8) ? 0u : static_cast<uint32_t>(brows * CG * TC_BK * 2);
     if (npre && leader) {
       const int n0 = (unit0 % nt) * bn + static_cast<int>(rank) * (bn / CG);
       int tr = 0, ts = 0, cb = 0;
@@ -309,9 +317,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (rank == 0) mbar_arrive_expect_tx(&full[kb], a_tx1 + b_tx1);
           uint8_t* dst = sB + kb * C::B_BYTES;
           if (CG == 2)
-            tma2_load_3d(dst, &wmap, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+            tma2_load_3d(dst, wm, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
           else
-            tma_load_3d(dst, &wmap, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+            tma_load_3d(dst, wm, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
         }
         if (++cb == cblocks) {
           cb = 0;
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const bool pre = g < npre;  // B already in flight, barrier armed
         if (leader && rank == 0 && !pre) {  // CG = 2: CTA 0's barrier counts both CTAs' bytes
           const uint32_t a_tx = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
-          const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(bn * TC_BK * 2);
+          const uint32_t b_tx = (p.dbg & 8) ? 0u : static_cast<uint32_t>(brows * CG * TC_BK * 2);
           const uint32_t tx = nsub * (a_tx + (RES_B ? 0u : b_tx));
           if (tx) mbar_arrive_expect_tx(&full[s], tx);
           else mbar_arrive(&full[s]);
@@ -388,9 +396,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (leader && !RES_B && !(p.dbg & 8) && !pre) {
               uint8_t* dst = sB + (s * KPS + j) * C::B_BYTES;
               if (CG == 2)
-                tma2_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+                tma2_load_3d(dst, wm, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
               else
-                tma_load_3d(dst, &wmap, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+                tma_load_3d(dst, wm, &full[s], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
             }
             if (++cb == cblocks) {
               cb = 0;

@@ -30,7 +30,24 @@ struct alignas(64) OpDesc {
   // 2-D tiled map over [rows][cout_a], box {32 columns, 128 rows} (conv_tc
   // RESB = 2 streams it through a shared-memory ring)
   CUtensorMap rmap;
+  // WeightSlice B operand of a tcgen05 conv at THIS subnet's tile width:
+  // box {64 ch, 1 tap, wrows} over the shared max-shape weights (wrows =
+  // the active tile width / CTAs per tile; 0 = use the graph's map)
+  CUtensorMap wmap;
+  int wrows;
 };
+
+// Active N-tile width of a tcgen05 conv: the graph-baked width bn_g (sized
+// for the max shape) shrinks to the active output width, keeping the tile
+// count, so a narrow subnet issues no MMA columns (and loads no weight rows)
+// past cout_a.  Multiples of 16 per CTA (MMA N granularity).
+__host__ __device__ __forceinline__ int conv_bn_active(int bn_g, int cout, int cg) {
+  const int q = 16 * cg;
+  const int nt = (cout + bn_g - 1) / bn_g;
+  int b = (cout + nt - 1) / nt;
+  b = (b + q - 1) / q * q;
+  return b < bn_g ? b : bn_g;
+}
 
 // GELU / tanh are out of line: inlined into the unrolled GEMM epilogues their
 // erff/tanhf bodies tripled the conv kernel's SASS and thrashed the I-cache.

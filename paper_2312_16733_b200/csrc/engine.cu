@@ -303,6 +303,44 @@ static int se_fused_parts(const ssn_engine* e, int di) {
   return dw_tiles_per_image(d.stride, d.hout, d.wout);
 }
 
+// Graph-independent parameters of conv op `oi` at `batch` images.
+static ConvParams conv_static_params(const ssn_engine* e, int oi, uint32_t batch) {
+  const OpSpec& o = e->net.ops[oi];
+  ConvParams p{};
+  p.n = static_cast<int>(batch);
+  p.h = o.hin;
+  p.w_ = o.win;
+  p.ho = o.hout;
+  p.wo = o.wout;
+  p.stride = o.stride;
+  p.M = static_cast<int>(batch) * o.hout * o.wout;
+  p.k_max = o.k_max;
+  p.cin_max = e->net.tensors[o.tensor].cin_store;
+  p.cout_max = o.cout_max;
+  p.act = o.act;
+  p.res_post = o.res_post;
+  p.out_f32 = o.kind == OP_LINEAR;
+  p.depthwise = o.depthwise;
+  return p;
+}
+
+// tcgen05 tiling of conv op `oi` (max-shape N width, split-K, pair tiles):
+// shared by graph capture and by subnet registration, which encodes each
+// subnet's weight map at the active tile width this tiling implies.
+static void conv_tc_tiling(const ssn_engine* e, int oi, ConvParams& p) {
+  const OpSpec& o = e->net.ops[oi];
+  const TensorSpec& t = e->net.tensors[o.tensor];
+  p.bn = choose_bn(o.cout_max, p.M, o.k_max * o.k_max * ((t.cin_store + 63) / 64));
+  // classifier head at <= 128 rows: one M tile, so the N width sets the
+  // CTA count — 64-wide tiles put 16 SMs (not 4) on the 32 K blocks
+  if (o.kind == OP_LINEAR && p.M <= 128 && o.cout_max > 64 && !(tc_debug_flags() & 262144))
+    p.bn = 64;
+  p.ws = e->d_ws;
+  p.rres = o.res != S_NONE && (o.cout_max & 7) == 0;  // every subnet's row carries rmap
+  p.splits = conv_tc_splits(p);
+  p.cg2 = p.splits > 1 ? 0 : conv_tc_use_pairs(p);
+}
+
 static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cudaStream_t s) {
   const OpSpec& o = e->net.ops[oi];
   const bool bf = e->bf16;
@@ -368,7 +406,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
         CUDA_TRY(launch_stem_conv(sp, s));
         return 1;
       }
-      ConvParams p{};
+      ConvParams p = conv_static_params(e, oi, batch);
       p.x = slot_ptr(e, o.in, map);
       p.y = slot_ptr(e, o.out, map);
       p.res = slot_ptr(e, o.res, map);
@@ -376,32 +414,10 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.row = e->d_rowptr;
       p.fixed = nullptr;
       p.op = oi;
-      p.n = static_cast<int>(batch);
-      p.h = o.hin;
-      p.w_ = o.win;
-      p.ho = o.hout;
-      p.wo = o.wout;
-      p.stride = o.stride;
-      p.M = static_cast<int>(batch) * o.hout * o.wout;
-      p.k_max = o.k_max;
-      p.cin_max = t.cin_store;
-      p.cout_max = o.cout_max;
-      p.act = o.act;
-      p.res_post = o.res_post;
-      p.out_f32 = o.kind == OP_LINEAR;
-      p.depthwise = o.depthwise;
       if (bf && use_halo(e, o)) {
         CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
       } else if (bf && !o.depthwise) {
-        p.bn = choose_bn(o.cout_max, p.M, o.k_max * o.k_max * ((t.cin_store + 63) / 64));
-        // classifier head at <= 128 rows: one M tile, so the N width sets the
-        // CTA count — 64-wide tiles put 16 SMs (not 4) on the 32 K blocks
-        if (o.kind == OP_LINEAR && p.M <= 128 && o.cout_max > 64 && !(tc_debug_flags() & 262144))
-          p.bn = 64;
-        p.ws = e->d_ws;
-        p.rres = p.res != nullptr && (o.cout_max & 7) == 0;  // every subnet's row carries rmap
-        p.splits = conv_tc_splits(p);
-        p.cg2 = p.splits > 1 ? 0 : conv_tc_use_pairs(p);
+        conv_tc_tiling(e, oi, p);
         CUtensorMap wmap{};
         if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout,
                             p.cg2 ? p.bn / 2 : p.bn) != 0)
@@ -661,6 +677,18 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
         if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
                          o.win, o.cin, o.k, o.stride, o.k / 2) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed for op " + std::to_string(oi));
+        // WeightSlice B at this subnet's tile width (largest-batch graph tiling)
+        if (!(tc_debug_flags() & 2097152)) {
+          ConvParams cp = conv_static_params(e, static_cast<int>(oi), e->desc.max_batch);
+          conv_tc_tiling(e, static_cast<int>(oi), cp);
+          const int cg = cp.cg2 ? 2 : 1;
+          const int bn_a = conv_bn_active(cp.bn, o.cout, cg);
+          const TensorSpec& t = e->net.tensors[o.tensor];
+          if (make_weight_map(&dsc.wmap, e->d_w + t.w_off, t.cin_store, o.k_max * o.k_max, t.cout,
+                              bn_a / cg) != 0)
+            SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (weights) failed for op " + std::to_string(oi));
+          dsc.wrows = bn_a / cg;
+        }
         // residual source for conv_tc's TMA residual ring
         if (res_ptr[oi] && (o.cout & 7) == 0 &&
             make_res_map(&dsc.rmap, res_ptr[oi],
