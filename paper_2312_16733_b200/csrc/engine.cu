@@ -57,7 +57,8 @@ cudaError_t launch_se(const SEParams& p, cudaStream_t s);
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s);
 cudaError_t launch_layernorm(const LnParams& p, cudaStream_t s);
 cudaError_t launch_token0(const Token0Params& p, cudaStream_t s);
-cudaError_t launch_attention(const AttnParams& p, int max_heads, cudaStream_t s);
+cudaError_t launch_attention(const AttnParams& p, int max_heads, bool tc, cudaStream_t s);
+int make_attn_map(CUtensorMap* map, const void* x, long rows, int c);
 }  // namespace ssn
 
 using namespace ssn;
@@ -482,7 +483,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.op = oi;
       p.n = static_cast<int>(batch);
       p.s = o.hin;
-      CUDA_TRY(launch_attention(p, o.cin_max / o.k_max, s));
+      CUDA_TRY(launch_attention(p, o.cin_max / o.k_max, bf && !(tc_debug_flags() & 8388608), s));
       return 1;
     }
     case OP_SE: {
@@ -643,6 +644,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
   // blocks are all skipped (LayerSelect) leaves its input where it is.
   std::vector<const void*> in_ptr(st.plan.ops.size(), nullptr);
   std::vector<const void*> res_ptr(st.plan.ops.size(), nullptr);
+  std::vector<const void*> in2_ptr(st.plan.ops.size(), nullptr), in3_ptr(st.plan.ops.size(), nullptr);
   bool flip = false;
   for (size_t si = 0; si < nseg; ++si) {
     st.seg_var[si] = st.seg_mask[si] | (flip ? SEG_FLIP : 0u);
@@ -652,6 +654,8 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     for (const SlotMap& sm : sp) {
       in_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in, sm.map);
       res_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].res, sm.map);
+      in2_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in2, sm.map);
+      in3_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in3, sm.map);
     }
   }
   std::vector<OpDesc> row(st.plan.ops.size());
@@ -659,6 +663,14 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     const OpSpec& o = st.plan.ops[oi];
     OpDesc& dsc = row[oi];
     std::memset(&dsc, 0, sizeof(dsc));
+    if (e->bf16 && o.active && o.kind == OP_ATTN) {
+      // tcgen05 attention: Q / K / V tiles of this subnet's active heads
+      const long rows = static_cast<long>(e->desc.max_batch) * o.hin;
+      if (make_attn_map(&dsc.amap, in_ptr[oi], rows, o.cin) != 0 ||
+          make_attn_map(&dsc.rmap, in2_ptr[oi], rows, o.cin) != 0 ||
+          make_attn_map(&dsc.wmap, in3_ptr[oi], rows, o.cin) != 0)
+        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (attention) failed for op " + std::to_string(oi));
+    }
     if (e->bf16 && o.active && o.kind == OP_CONV && o.depthwise) {
       // depthwise input window map (box sized for this subnet's k)
       if (make_dw_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,

@@ -237,6 +237,245 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnParams p) {
   }
 }
 
+// ---------------------------------------------------------------- attention (tcgen05)
+// Persistent, warp-specialised: one CTA per SM walks (sequence, active head)
+// units with two buffers of everything, so unit i+1's Q/K/V loads and S MMA
+// overlap unit i's softmax and P.V.
+//  * warp 0: TMA — Q, K, V of a unit are three {64 dims, 128 rows} SW128 boxes
+//    of the subnet's [n*s][C_a] activations (maps in the op's OpDesc row:
+//    amap = Q, rmap = K, wmap = V);
+//  * warp 1: MMA issuer — S = Q K^T (M = N = 128, K = 64; both operands
+//    K-major) into TMEM, then O = P V (M = 128, N = 64, K = 128; P K-major
+//    from shared memory, V read MN-major straight from its TMA tile);
+//  * warps 4-7 (even units, buffer 0) and 8-11 (odd units, buffer 1): one
+//    thread per query row — tcgen05.ld of its 128 scores,
+//    max / exp / sum in registers (no shuffles), P in bf16 written SW128
+//    K-major for the second MMA, then O / l from TMEM to global.
+// TMEM: S of buffer b at columns [128 b, 128 b + 128), O at 256 + 64 b.
+constexpr int ATC_UNIT_SMEM = 80 * 1024;  // Q 16 KB | K 16 KB | V 16 KB | P 32 KB
+constexpr int ATC_SMEM = 2 * ATC_UNIT_SMEM + 1024 + 256;
+
+__device__ __forceinline__ uint64_t umma_desc_sw128_at(uint32_t addr) { return umma_desc_sw128(addr); }
+
+constexpr int ATC_THREADS = 384;
+
+__global__ void __launch_bounds__(ATC_THREADS, 1) attention_tc_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * ATC_UNIT_SMEM);
+  uint64_t* kv_full = bar;       // [2] TMA landed Q, K, V
+  uint64_t* kv_empty = bar + 2;  // [2] P.V of the buffer's last unit done (Q/K/V/P free)
+  uint64_t* s_full = bar + 4;    // [2] S in TMEM
+  uint64_t* s_empty = bar + 6;   // [2] S read out by the softmax warps
+  uint64_t* p_full = bar + 8;    // [2] P in shared memory
+  uint64_t* o_full = bar + 10;   // [2] O in TMEM
+  uint64_t* o_empty = bar + 12;  // [2] O read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  pdl_wait();
+  pdl_trigger();
+  const OpDesc* dp = desc_ptr(p.row, nullptr, p.op);
+  const int C = dp->cin;
+  const int heads = C / ATT_D;
+  const int units = p.n * heads;
+  if (static_cast<int>(blockIdx.x) >= units) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&kv_full[b], 1);
+      mbar_init(&kv_empty[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 4);  // the four softmax warps
+      mbar_init(&p_full[b], 4);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch(&dp->amap);
+    tma_prefetch(&dp->rmap);
+    tma_prefetch(&dp->wmap);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int step = static_cast<int>(gridDim.x);
+
+  if (warp == 0) {
+    // ============================================================ TMA producer
+    const bool leader = elect_one();
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += step, ++i) {
+      const int b = i & 1;
+      const uint32_t ph = (i >> 1) & 1;
+      const int seq = u / heads, h = u - seq * heads;
+      mbar_wait(&kv_empty[b], ph ^ 1);
+      if (leader) {
+        uint8_t* base = smem + b * ATC_UNIT_SMEM;
+        mbar_arrive_expect_tx(&kv_full[b], 3 * ATT_S * ATT_D * 2);
+        tma_load_2d(base, &dp->amap, &kv_full[b], h * ATT_D, seq * ATT_S);
+        tma_load_2d(base + 16384, &dp->rmap, &kv_full[b], h * ATT_D, seq * ATT_S);
+        tma_load_2d(base + 32768, &dp->wmap, &kv_full[b], h * ATT_D, seq * ATT_S);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ============================================================ MMA issuer
+    const uint32_t idesc_s = umma_idesc_bf16(ATT_S, 128);
+    const uint32_t idesc_o = umma_idesc_bf16(ATT_D, 128) | (1u << 16);  // B (V) MN-major
+    const int count = (units - static_cast<int>(blockIdx.x) + step - 1) / step;
+    auto mma_s = [&](int i) {
+      const int b = i & 1;
+      const uint32_t ph = (i >> 1) & 1;
+      mbar_wait(&kv_full[b], ph);
+      mbar_wait(&s_empty[b], ph ^ 1);
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + b * ATC_UNIT_SMEM);
+      const uint64_t qd = umma_desc_sw128_at(base), kd = umma_desc_sw128_at(base + 16384);
+#pragma unroll
+      for (int kk = 0; kk < ATT_D / 16; ++kk)
+        tc_mma_bf16_elect(tmem + b * 128, qd + kk * 2, kd + kk * 2, idesc_s, kk ? 1u : 0u);
+      tc_commit_elect(&s_full[b]);
+      __syncwarp();
+    };
+    if (count > 0) mma_s(0);
+    for (int i = 0; i < count; ++i) {
+      if (i + 1 < count) mma_s(i + 1);
+      const int b = i & 1;
+      const uint32_t ph = (i >> 1) & 1;
+      mbar_wait(&p_full[b], ph);
+      mbar_wait(&o_empty[b], ph ^ 1);
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + b * ATC_UNIT_SMEM);
+      const uint64_t pd = umma_desc_sw128_at(base + 49152);
+      const uint64_t vd = umma_desc_sw128_at(base + 32768);
+#pragma unroll
+      for (int kk = 0; kk < ATT_S / 16; ++kk)
+        tc_mma_bf16_elect(tmem + 256 + b * 64,
+                          pd + static_cast<uint64_t>((kk >> 2) * (16384 >> 4) + (kk & 3) * 2),
+                          vd + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_o, kk ? 1u : 0u);
+      tc_commit_elect(&o_full[b]);
+      tc_commit_elect(&kv_empty[b]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ============================================================ softmax + epilogue
+    const int quarter = warp & 3;
+    const int wg = (warp - 4) >> 2;     // warpgroup = buffer = unit parity
+    const int r = quarter * 32 + lane;  // query row
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.o);
+    int i = wg;
+    for (int u = blockIdx.x + wg * step; u < units; u += 2 * step, i += 2) {
+      const int b = i & 1;
+      const uint32_t ph = (i >> 1) & 1;
+      const int seq = u / heads, h = u - seq * heads;
+      mbar_wait(&s_full[b], ph);
+      tc_fence_after();
+      float sv[ATT_S];
+#pragma unroll
+      for (int c = 0; c < ATT_S / 32; ++c) {
+        float t[32];
+        tmem_ld32(tmem + lane_off + b * 128 + c * 32, t);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sv[c * 32 + j] = t[j];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);
+      float m = sv[0];
+#pragma unroll
+      for (int j = 1; j < ATT_S; ++j) m = fmaxf(m, sv[j]);
+      const float scale = 0.125f;  // 1/sqrt(64)
+      float l = 0.f;
+#pragma unroll
+      for (int j = 0; j < ATT_S; ++j) {
+        sv[j] = __expf((sv[j] - m) * scale);
+        l += sv[j];
+      }
+      // P row r, SW128 K-major: key block kb (64 keys, 16 KB), 16-byte chunk
+      // c of the 128-byte row lands at chunk c ^ (r % 8)
+      uint8_t* pb = smem + b * ATC_UNIT_SMEM + 49152 + r * 128;
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float* e = sv + kb * 64 + c * 8;
+          uint4 v;
+          v.x = pack_bf16x2(e[0], e[1]);
+          v.y = pack_bf16x2(e[2], e[3]);
+          v.z = pack_bf16x2(e[4], e[5]);
+          v.w = pack_bf16x2(e[6], e[7]);
+          *reinterpret_cast<uint4*>(pb + kb * 16384 + ((c ^ (r & 7)) << 4)) = v;
+        }
+      fence_proxy_async_smem();  // generic-proxy P stores -> the tensor core's reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      // O = P V / l
+      mbar_wait(&o_full[b], ph);
+      tc_fence_after();
+      float o[ATT_D];
+#pragma unroll
+      for (int c = 0; c < ATT_D / 32; ++c) {
+        float t[32];
+        tmem_ld32(tmem + lane_off + 256 + b * 64 + c * 32, t);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[c * 32 + j] = t[j];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[b]);
+      const float il = 1.f / l;
+      uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<long>(seq) * ATT_S + r) * C + h * ATT_D);
+#pragma unroll
+      for (int c = 0; c < ATT_D / 8; ++c) {
+        uint4 v;
+        v.x = pack_bf16x2(o[c * 8 + 0] * il, o[c * 8 + 1] * il);
+        v.y = pack_bf16x2(o[c * 8 + 2] * il, o[c * 8 + 3] * il);
+        v.z = pack_bf16x2(o[c * 8 + 4] * il, o[c * 8 + 5] * il);
+        v.w = pack_bf16x2(o[c * 8 + 6] * il, o[c * 8 + 7] * il);
+        dst[c] = v;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Q / K / V source of the tcgen05 attention: [rows][c] bf16 (c = active
+// heads x 64), box {64 columns, 128 rows}, 128-byte swizzle (UMMA K-major
+// for Q and K; V is read MN-major from the same layout).
+int make_attn_map(CUtensorMap* map, const void* x, long rows, int c) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                          CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                          CUtensorMapFloatOOBfill);
+  static Fn enc = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<Fn>(ptr);
+    return static_cast<Fn>(nullptr);
+  }();
+  if (!enc || c % ATT_D != 0) return -1;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(c) * 2};
+  cuuint32_t box[2] = {ATT_D, ATT_S};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
   const long warps = static_cast<long>(p.n) * p.s;
@@ -259,9 +498,26 @@ cudaError_t launch_token0(const Token0Params& p, cudaStream_t s) {
   return launch_pdl(token0_kernel, dim3((p.n * (p.c / 8) + 255) / 256), dim3(256), 0, s, 1, p);
 }
 
-// grid = n x max heads; CTAs past the active head count exit
-cudaError_t launch_attention(const AttnParams& p, int max_heads, cudaStream_t s) {
+// tcgen05 path (engine rows carry the Q/K/V maps): persistent, one CTA per
+// SM; `SSN_TC_DEBUG & 8388608` or a row without maps -> the mma.sync kernel
+// (grid = n x max heads; CTAs past the active head count exit).
+cudaError_t launch_attention(const AttnParams& p, int max_heads, bool tc, cudaStream_t s) {
   if (p.s != ATT_S) return cudaErrorInvalidValue;
+  if (tc) {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATC_SMEM);
+    if (attr != cudaSuccess) return attr;
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const int units = p.n * max_heads;
+    return launch_pdl(attention_tc_kernel, dim3(units < sms ? units : sms), dim3(ATC_THREADS),
+                      ATC_SMEM, s, 1, p);
+  }
   return launch_pdl(attention_kernel, dim3(p.n * max_heads), dim3(256), 0, s, 1, p);
 }
 
