@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 OUT = os.path.join(HERE, "libssn.so")
-SOURCES = ["engine.cu", "conv_tc.cu", "conv_halo.cu", "kernels.cu", "dw.cu", "transformer.cu"]
+SOURCES = ["engine.cu", "conv_tc.cu", "conv_halo.cu", "conv_hp.cu", "kernels.cu", "dw.cu", "transformer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,399 @@
+// conv_hp.cu — stride-1 3x3 WeightSlice convolution for WIDE layers as a
+// shifted-window ("halo") implicit GEMM on 2-CTA tcgen05 pairs (sm_100a):
+// OFA-ResNet50's 3x3 convs at 28 and 14 px (104-360 active channels).
+//
+// Why (profiles/round2): conv_tc feeds these layers with TMA
+// im2col boxes — every K block re-reads 128 output pixels x 64 channels per
+// filter tap, 9 boxes per channel block, 128 pixel requests each.  Measured
+// on B200, the loads alone (SSN_TC_DEBUG=2, no MMA) take as long as the whole
+// layer: the im2col request stream, not the tensor core, bounds it.  Here:
+//  * the A window map is the subnet row's `rmap` slot (these convs have no
+//    residual; `amap` keeps conv_tc's im2col map for the small-batch graphs);
+//  * output positions are taken in padded-width order (HaloGeom, Wp = W + 2):
+//    tap (r, s) of position p reads window pixel p + r*Wp + s, so ONE tiled
+//    TMA box per 64-channel block — the halo window, rows of 128 B, SW128 —
+//    feeds all 9 taps: each tap's A operand is the same window at a row
+//    offset (any 128-B row offset is a legal SW128 K-major start,
+//    tools/ubench/sw128_shift.cu);
+//  * a CTA tile is RT whole padded rows (<= 128 positions) of one image; a
+//    cluster of two CTAs computes two such tiles (consecutive in the
+//    (image, row-block) order) as ONE M = 256 tcgen05.mma.cta_group::2, each
+//    CTA holding its own window and HALF of the weight rows;
+//  * B (the WeightSlice of one (channel block, tap)) streams through a ring
+//    of {64 ch, 1 tap, bn/2 rows} boxes from the max-shape KRSC tensor;
+//  * garbage positions (2 padding columns per row, rows past H) are computed
+//    and dropped by the epilogue: 196/256 of the MMA rows are live at 14 px,
+//    784/896 at 28 px.
+// Warp roles (512 threads): warp 0 window producer, warp 1 MMA issuer (CTA 0
+// of the pair), warps 2-3 weight producers (alternate stages), warps 4-15 the
+// epilogue (TMEM -> padded smem transpose -> SubnetNorm + activation on
+// coalesced 64-byte row segments), as conv_tc.  Two TMEM accumulators.
+#include <cstdio>
+#include <cstdlib>
+
+#include "device.cuh"
+
+namespace ssn {
+
+constexpr int HP_BN_MAX = 256;
+constexpr int HP_THREADS = 512;
+constexpr int HP_EPI_WARP0 = 4;
+constexpr int HP_EPI_WARPS = 12;
+constexpr int HP_EPI_GROUPS = 3;
+constexpr int HP_STG_LD = 36;
+constexpr int HP_STG_BYTES = HP_EPI_WARPS * 32 * HP_STG_LD * 4;
+constexpr int HP_B_STAGE = HP_BN_MAX / 2 * 128;  // one CTA's half of a (block, tap) B box
+constexpr int HP_SMEM_MAX = 232448;
+constexpr int HP_NACC = 2;
+
+__host__ __device__ __forceinline__ int hp_window_bytes(int w) {
+  const HaloGeom g = halo_geom(w, 3);
+  return g.r * g.wp * 128;
+}
+__host__ __device__ __forceinline__ int hp_window_slot(int w) {
+  return (hp_window_bytes(w) + 1023) & ~1023;
+}
+
+__global__ void __launch_bounds__(HP_THREADS, 1)
+    conv_hp_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const HaloGeom hg = halo_geom(p.w_, 3);
+  const int wp = hg.wp, rt = hg.rt;
+  const int wslot = hp_window_slot(p.w_);
+  const uint32_t wbytes = static_cast<uint32_t>(hp_window_bytes(p.w_));
+  const int SB = p.h_stages;  // B ring depth
+  uint8_t* sW = smem;                         // [2] halo windows
+  uint8_t* sB = smem + 2 * wslot;             // [SB] B half-boxes
+  float* stg = reinterpret_cast<float*>(sB + SB * HP_B_STAGE);
+  uint64_t* afull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + HP_STG_BYTES);
+  uint64_t* aempty = afull + 2;
+  uint64_t* bfull = aempty + 2;
+  uint64_t* bempty = bfull + SB;
+  uint64_t* tfull = bempty + SB;
+  uint64_t* tempty = tfull + HP_NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + HP_NACC);
+
+  const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
+  const OpDims d = load_desc(p.row, p.fixed, p.op);
+  const int bn = conv_bn_active(p.bn, d.cout, 2);
+  // the subnet row's wmap is sized for conv_tc's tiling of this op; it is
+  // used when its box width happens to match, else the graph's max-width map
+  // (rows past the active width land unused)
+  const bool own_wmap = dp->wrows == bn / 2;
+  const CUtensorMap* wm = own_wmap ? &dp->wmap : &wmap;
+  const int brows = own_wmap ? bn / 2 : p.bn / 2;
+  const int nt = (d.cout + bn - 1) / bn;
+  const int tpi = (p.h + rt - 1) / rt;           // CTA tiles per image
+  const int pairs = (p.n * tpi + 1) / 2;          // pair tiles (2 CTA tiles each)
+  const int units = pairs * nt;
+  const uint32_t rank = cluster_rank();
+  const int u0 = static_cast<int>(blockIdx.x) / 2, ustep = static_cast<int>(gridDim.x) / 2;
+  if (u0 >= units) return;  // both CTAs of a pair agree
+  const int ncb = (d.cin + 63) / 64;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&afull[i], 1);
+      mbar_init(&aempty[i], 1);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int a = 0; a < HP_NACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], HP_EPI_WARPS * 2);  // both CTAs' epilogue warps
+    }
+    fence_mbar_init();
+    tma_prefetch(wm);
+    tma_prefetch(&dp->rmap);
+  }
+  if (warp == 1) tmem2_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+
+  // CTA tile q -> (image, first output row); tile index past the batch = idle half
+  auto tile_of = [&](int u, int& img, int& r0) {
+    const int q = (u / nt) * 2 + static_cast<int>(rank);
+    img = q / tpi;
+    r0 = (q - img * tpi) * rt;
+  };
+
+  if (warp == 0) {
+    // ====================================================== window producer
+    const bool leader = elect_one();
+    pdl_wait();
+    int g = 0;
+    for (int u = u0; u < units; u += ustep) {
+      int img, r0;
+      tile_of(u, img, r0);
+      for (int cb = 0; cb < ncb; ++cb, ++g) {
+        const int w = g & 1;
+        mbar_wait(&aempty[w], ((g >> 1) & 1) ^ 1);
+        if (leader) {
+          if (p.dbg & 4) {  // profiling: no window loads
+            if (rank == 0) mbar_arrive(&afull[w]);
+          } else {
+            if (rank == 0) mbar_arrive_expect_tx(&afull[w], 2 * wbytes);
+            tma2_load_4d(sW + w * wslot, &dp->rmap, &afull[w], cb * 64, -1, r0 - 1, img);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ====================================================== weight producers
+    const int pidx = warp - 2;
+    const bool leader = elect_one();
+    const uint32_t btx = static_cast<uint32_t>(brows) * 128 * 2;
+    int h = 0;
+    for (int u = u0; u < units; u += ustep) {
+      const int n0 = (u % nt) * bn + static_cast<int>(rank) * (bn / 2);
+      for (int cb = 0; cb < ncb; ++cb)
+        for (int tap = 0; tap < 9; ++tap, ++h) {
+          if ((h & 1) != pidx) continue;
+          const int s = h % SB;
+          mbar_wait(&bempty[s], ((h / SB) & 1) ^ 1);
+          if (leader && (p.dbg & 8)) {  // profiling: no weight loads
+            if (rank == 0) mbar_arrive(&bfull[s]);
+          } else if (leader) {
+            if (rank == 0) mbar_arrive_expect_tx(&bfull[s], btx);
+            tma2_load_3d(sB + s * HP_B_STAGE, wm, &bfull[s], cb * 64,
+                         (tap / 3 + (p.k_max - 3) / 2) * p.k_max + tap % 3 + (p.k_max - 3) / 2, n0);
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == 1) {
+    // ====================================================== MMA issuer (CTA 0)
+    if (rank == 0) {
+      const uint32_t idesc = umma_idesc_bf16(bn, 256);
+      const uint64_t a_base = umma_desc_sw128(smem_u32(sW));
+      const uint64_t b_base = umma_desc_sw128(smem_u32(sB));
+      int g = 0, h = 0, i = 0;
+      for (int u = u0; u < units; u += ustep, ++i) {
+        const int a = i & 1;
+        mbar_wait(&tempty[a], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + a * HP_BN_MAX;
+        for (int cb = 0; cb < ncb; ++cb, ++g) {
+          const int w = g & 1;
+          mbar_wait(&afull[w], (g >> 1) & 1);
+          const int nks = min(4, (d.cin - cb * 64 + 15) / 16);
+          const uint64_t ad = a_base + static_cast<uint64_t>((w * wslot) >> 4);
+          for (int tap = 0; tap < 9; ++tap, ++h) {
+            const int s = h % SB;
+            mbar_wait(&bfull[s], (h / SB) & 1);
+            tc_fence_after();
+            const uint64_t at = ad + static_cast<uint64_t>(((tap / 3) * wp + tap % 3) * 8);
+            const uint64_t bd = b_base + static_cast<uint64_t>((s * HP_B_STAGE) >> 4);
+            for (int kk = 0; kk < nks && !(p.dbg & 2); ++kk)
+              tc2_mma_bf16_elect(acc, at + static_cast<uint64_t>(kk * 2),
+                                 bd + static_cast<uint64_t>(kk * 2), idesc,
+                                 (cb | tap | kk) != 0 ? 1u : 0u);
+            tc2_commit_mc_elect(&bempty[s]);
+            __syncwarp();
+          }
+          tc2_commit_mc_elect(&aempty[w]);  // window w free once its 9 taps retire
+          __syncwarp();
+        }
+        tc2_commit_mc_elect(&tfull[a]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ====================================================== epilogue
+    pdl_wait();
+    const int ew = warp - HP_EPI_WARP0;
+    const int quarter = warp & 3;
+    const int group = ew >> 2;
+    float* st = stg + ew * (32 * HP_STG_LD);
+    const int seg = lane & 3, rsub = lane >> 2;
+    const int nchunk = (bn + 31) / 32;
+    const bool relu = p.act == 1;
+    int i = 0;
+    for (int u = u0; u < units; u += ustep, ++i) {
+      const int a = i & 1;
+      int img, r0;
+      tile_of(u, img, r0);
+      const int nb = (u % nt) * bn;
+      const int nch = min(nchunk, (d.cout - nb + 31) / 32);
+      mbar_wait(&tfull[a], (i >> 1) & 1);
+      tc_fence_after();
+      for (int c = group; c < nch; c += HP_EPI_GROUPS) {
+        const int col = nb + c * 32 + seg * 8;
+        const bool colok = col < d.cout && c * 32 + seg * 8 < bn;
+        float sc[8], sh[8];
+        if (colok) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            sc[q] = d.scale ? __ldg(d.scale + col + q) : 1.f;
+            sh[q] = d.shift ? __ldg(d.shift + col + q) : 0.f;
+          }
+        }
+        float v[32];
+        tmem_ld32(tmem + a * HP_BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+        float4* srow = reinterpret_cast<float4*>(st + lane * HP_STG_LD);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) srow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
+        if (colok && !(p.dbg & 1)) {
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4) {
+            const int pos = quarter * 32 + rsub + 8 * r4;  // padded-width position in the CTA tile
+            const int rr = pos / wp, cc = pos - rr * wp;
+            const int oh = r0 + rr;
+            if (rr >= rt || cc >= p.wo || oh >= p.ho || img >= p.n) continue;
+            const float4* sp = reinterpret_cast<const float4*>(st + (rsub + 8 * r4) * HP_STG_LD + seg * 8);
+            const float4 lo = sp[0], hi = sp[1];
+            float o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              o[q] = o[q] * sc[q] + sh[q];
+              if (relu) o[q] = fmaxf(o[q], 0.f);
+            }
+            uint4 pk;
+            pk.x = pack_bf16x2(o[0], o[1]);
+            pk.y = pack_bf16x2(o[2], o[3]);
+            pk.z = pack_bf16x2(o[4], o[5]);
+            pk.w = pack_bf16x2(o[6], o[7]);
+            const size_t m = (static_cast<size_t>(img) * p.ho + oh) * p.wo + cc;
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + m * d.cout + col) = pk;
+          }
+        }
+        __syncwarp();  // staging tile is rewritten by the next chunk
+      }
+      // accumulator a drained by this warp (both CTAs' warps arrive on CTA 0)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(&tempty[a], 0));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem2_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+using EncodeTiledFnP = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFnP hp_encoder() {
+  static EncodeTiledFnP fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<EncodeTiledFnP>(ptr);
+    return static_cast<EncodeTiledFnP>(nullptr);
+  }();
+  return fn;
+}
+
+static int hp_b_stages(int w) {
+  const long avail = HP_SMEM_MAX - 1024 - 2L * hp_window_slot(w) - HP_STG_BYTES - 256;
+  const long st = avail / HP_B_STAGE;
+  return static_cast<int>(st > 8 ? 8 : st);
+}
+
+// Wide stride-1 3x3 convs whose max width exceeds the resident-weight halo
+// kernel (conv_halo: cout <= 128).  k_max 3 only (OFA-ResNet50).  Measured
+// (ncu device time, tools/microbench_conv.py, profiles/round2/README.md): at
+// 14 px it beats conv_tc's im2col path (360 ch bs64 46 vs 53 us, bs256 141 vs
+// 172 us); at 28 px it loses (176 ch 46 vs 38 us: 87.5% live rows and a
+// ragged last wave of pair tiles), so the graph uses it up to 20 px only
+// (SSN_HP_MAX_W overrides for experiments; the operator API, graph = false,
+// takes any width so the parity tests cover the 28-px geometry).
+bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max, bool graph) {
+  static const bool off = [] {
+    const char* e = getenv("SSN_NO_HP");  // A/B switch for profiling
+    return e && atoi(e) != 0;
+  }();
+  static const int max_w = [] {
+    const char* e = getenv("SSN_HP_MAX_W");
+    return e ? atoi(e) : 20;
+  }();
+  if (off || stride != 1 || k_max != 3 || h < 8 || w < 12 || w > 62 || (graph && w > max_w)) return false;
+  if (cout_max <= 128 || (cout_max & 7) != 0 || (cin_max & 7) != 0) return false;
+  return hp_b_stages(w) >= 3;
+}
+
+// A operand: [n][h][w][cin_a] NHWC bf16, box {64 ch, Wp, R, 1}, 128-byte
+// swizzle: one halo window of one 64-channel block as 128-B pixel rows.
+int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin) {
+  EncodeTiledFnP enc = hp_encoder();
+  if (!enc || (cin & 7) != 0) return -1;
+  const HaloGeom g = halo_geom(w, 3);
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
+                        static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(w) * cin * 2,
+                           static_cast<cuuint64_t>(h) * w * cin * 2};
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(g.wp), static_cast<cuuint32_t>(g.r), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
+}
+
+// N tile of a pair: the active width in <= 256-wide, 32-aligned tiles
+int hp_choose_bn(int cout_max) {
+  const int nt = (cout_max + HP_BN_MAX - 1) / HP_BN_MAX;
+  const int b = (cout_max + nt - 1) / nt;
+  return (b + 31) / 32 * 32;
+}
+
+static int hp_sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+cudaError_t init_conv_hp() {
+  return cudaFuncSetAttribute(conv_hp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              HP_SMEM_MAX);
+}
+
+// p: the op's max geometry + graph-baked batch, p.bn = hp_choose_bn(cout_max);
+// wmap: max-width weight map with bn / 2 rows per box.
+cudaError_t launch_conv_hp(ConvParams p, const CUtensorMap& wmap, cudaStream_t s) {
+  static const int dbg = [] {
+    const char* e = getenv("SSN_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  p.dbg = dbg;
+  p.h_stages = hp_b_stages(p.w_);
+  if (p.h_stages < 3 || p.ho != p.h || p.wo != p.w_) return cudaErrorInvalidValue;
+  const long smem = 1024 + 2L * hp_window_slot(p.w_) + static_cast<long>(p.h_stages) * HP_B_STAGE +
+                    HP_STG_BYTES + (4 + 2 * p.h_stages + 2 * HP_NACC) * 8 + 16;
+  const HaloGeom g = halo_geom(p.w_, 3);
+  const long pairs = (static_cast<long>(p.n) * ((p.h + g.rt - 1) / g.rt) + 1) / 2;
+  const long units = pairs * ((p.cout_max + p.bn - 1) / p.bn);
+  const long slots = hp_sm_count() / 2;
+  const long np = units < slots ? units : slots;
+  return launch_pdl(conv_hp_kernel, dim3(static_cast<unsigned>(np * 2)), dim3(HP_THREADS),
+                    static_cast<size_t>(smem), s, 2, p, wmap);
+}
+
+}  // namespace ssn

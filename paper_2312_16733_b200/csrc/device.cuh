@@ -475,6 +475,15 @@ __device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* map, 
       "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma2_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                             int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void tma2_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c,
                                                int w, int h, int n, uint16_t off_w, uint16_t off_h) {
   asm volatile(

@@ -43,6 +43,11 @@ cudaError_t init_conv_halo();
 bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max);
 int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k);
 cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps, cudaStream_t s);
+cudaError_t init_conv_hp();
+bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max, bool graph);
+int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin);
+int hp_choose_bn(int cout_max);
+cudaError_t launch_conv_hp(ConvParams p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t launch_input(const InputParams& p, cudaStream_t s);
 cudaError_t launch_stem_conv(const StemParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t s);
@@ -272,6 +277,20 @@ static bool use_halo(const ssn_engine* e, const OpSpec& o) {
   return halo_eligible(o.hin, o.win, o.k_max, o.stride, t.cin_store, o.cout_max);
 }
 
+// Wider stride-1 3x3 convs without a residual (OFA-R50 3x3 at 28 / 14 px)
+// run the 2-CTA shifted-window kernel (conv_hp.cu); same max-shape rule.
+static bool use_hp(const ssn_engine* e, const OpSpec& o, uint32_t batch) {
+  // small batches: conv_tc's split-K spreads the few tiles better (bs1 max
+  // 630 vs 665 us); from 32 images on the pair kernel wins (bs256 max -1.6%)
+  if (batch < 32) return false;
+  if (!e->bf16 || o.kind != OP_CONV || o.depthwise || o.act > 1 || o.res != S_NONE ||
+      (o.cout_max & 7) != 0 || use_halo(e, o))
+    return false;
+  const TensorSpec& t = e->net.tensors[o.tensor];
+  if (t.im2col_stem) return false;
+  return hp_eligible(o.hin, o.win, o.k_max, o.stride, t.cin_store, o.cout_max, true);
+}
+
 static int tc_debug_flags() {  // SSN_TC_DEBUG & 65536: unfused stem (profiling only)
   static const int v = [] {
     const char* e = getenv("SSN_TC_DEBUG");
@@ -417,6 +436,12 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       p.op = oi;
       if (bf && use_halo(e, o)) {
         CUDA_TRY(launch_conv_halo(p, p.w, t.cin_store, o.k_max * o.k_max, s));
+      } else if (bf && use_hp(e, o, batch)) {
+        p.bn = hp_choose_bn(o.cout_max);
+        CUtensorMap wmap{};
+        if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn / 2) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
+        CUDA_TRY(launch_conv_hp(p, wmap, s));
       } else if (bf && !o.depthwise) {
         conv_tc_tiling(e, oi, p);
         CUtensorMap wmap{};
@@ -701,6 +726,14 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
             SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (weights) failed for op " + std::to_string(oi));
           dsc.wrows = bn_a / cg;
         }
+        // shifted-window pair kernel (large-batch graphs of residual-free
+        // 14-px 3x3 convs): its 4-D window map rides in the unused rmap slot
+        // (B comes from the graph's max-width map), so the same subnet row
+        // also serves the small-batch graphs' conv_tc
+        if (use_hp(e, o, e->desc.max_batch) &&
+            make_hp_act_map(&dsc.rmap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
+                            o.win, o.cin) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (hp) failed for op " + std::to_string(oi));
         // residual source for conv_tc's TMA residual ring
         if (res_ptr[oi] && (o.cout & 7) == 0 &&
             make_res_map(&dsc.rmap, res_ptr[oi],
@@ -828,6 +861,7 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     if (e->bf16) {
       CUDA_TRY(init_conv_tc());
       CUDA_TRY(init_conv_halo());
+      CUDA_TRY(init_conv_hp());
     }
     std::vector<uint8_t> gen;
     const uint8_t* blob = static_cast<const uint8_t*>(host_weights);
@@ -1260,14 +1294,18 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(init_conv_tc());
     CUDA_TRY(init_conv_halo());
+    CUDA_TRY(init_conv_hp());
     const bool aligned16 =
         ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) == 0;
     const bool halo = pad == k / 2 && !out_f32 && act <= 1 && (cout & 7) == 0 &&
                       (cout_max & 7) == 0 && aligned16 &&
                       halo_eligible(h, w, k, stride, cin_max, cout_max);
+    const bool hp = !halo && pad == k / 2 && !out_f32 && act <= 1 && !res && (cout & 7) == 0 &&
+                    (cout_max & 7) == 0 && aligned16 && !(getenv("SSN_OP_NO_HP")) &&
+                    hp_eligible(h, w, k, stride, cin_max, cout_max, false);
     OpDesc d = plain_desc(cin, cout, k, pad, scale, shift);
-    if (halo ? make_halo_act_map(&d.amap, x, n, h, w, cin, k) != 0
-             : make_act_map(&d.amap, x, n, h, w, cin, k, stride, pad) != 0)
+    if (!hp && (halo ? make_halo_act_map(&d.amap, x, n, h, w, cin, k) != 0
+                     : make_act_map(&d.amap, x, n, h, w, cin, k, stride, pad) != 0))
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncode (activation) failed");
     ConvParams p{};
     p.x = x;
@@ -1291,6 +1329,21 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     p.out_f32 = out_f32;
     if (halo) {
       CUDA_TRY(launch_conv_halo(p, wgt, cin_max, k * k, s));
+      return;
+    }
+    if (hp) {
+      p.bn = hp_choose_bn(cout_max);
+      const int bn_a = conv_bn_active(p.bn, cout, 2);
+      OpDesc d2 = d;
+      if (make_hp_act_map(&d2.rmap, x, n, h, w, cin) != 0 ||
+          make_weight_map(&d2.wmap, wgt, cin_max, k * k, cout_max, bn_a / 2) != 0)
+        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncode (hp) failed");
+      d2.wrows = bn_a / 2;
+      p.fixed = op_desc_scratch(d2, s);
+      CUtensorMap wmap{};
+      if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn / 2) != 0)
+        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
+      CUDA_TRY(launch_conv_hp(p, wmap, s));
       return;
     }
     p.bn = choose_bn(cout_max, p.M, k * k * ((cin_max + 63) / 64));

@@ -81,6 +81,15 @@ CASES = [
     (3, 28, 28, 40, 64, 48, 64, 3, 1),      # cin16 = 48: a half channel block
     (2, 20, 30, 16, 16, 16, 16, 3, 1),      # h != w, 4 rows per tile
     (5, 17, 19, 32, 32, 64, 64, 3, 1),      # odd sizes, last tile past H
+    # shifted-window PAIR kernel (conv_hp.cu): wide stride-1 3x3 at 14-62 px
+    (2, 14, 14, 360, 360, 360, 360, 3, 1),  # OFA-R50 stage-3 max (2 N tiles of 192/168)
+    (3, 14, 14, 208, 360, 208, 360, 3, 1),  # WeightSlice of the max tensor, odd CTA-tile count
+    (1, 28, 28, 176, 176, 176, 176, 3, 1),  # 7 CTA tiles: idle half in the last pair
+    (2, 28, 28, 104, 176, 104, 176, 3, 1),  # mid-subnet stage 2
+    (5, 14, 14, 136, 360, 136, 360, 3, 1),  # min-subnet stage 3, ragged K block
+    (2, 20, 30, 144, 144, 160, 160, 3, 1),  # h != w (Wp 32, 4 rows per CTA tile)
+    (1, 14, 14, 40, 360, 360, 360, 3, 1),   # one partial channel block
+    (2, 14, 14, 360, 360, 512, 512, 3, 1),  # 2 full 256-wide N tiles
 ]
 
 

@@ -47,6 +47,13 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (64, 14, 14, 1024, 1024, 360, 360, 1, 1, 0),     # 32: stage-3 reduce
     (64, 112, 112, 32, 32, 64, 64, 3, 1, 0),         # 33: max stem 3x3 32->64 (halo)
     (64, 112, 112, 32, 32, 32, 32, 3, 1, 1),         # 34: stem residual block (halo + residual)
+    (64, 14, 14, 368, 368, 368, 368, 3, 1, 0),       # 35: case2 at a 32-B aligned width
+    (64, 7, 7, 768, 768, 768, 768, 3, 1, 0),         # 36: case6 at a 128-B aligned width
+    (64, 28, 28, 192, 192, 192, 192, 3, 1, 0),       # 37: case8 at a 128-B aligned width
+    (64, 14, 14, 352, 352, 352, 352, 3, 1, 0),       # 38: 32-B aligned, narrower than case2
+    (64, 14, 14, 1024, 1024, 368, 368, 1, 1, 0),     # 39: = case32 at a 32-B aligned width
+    (64, 14, 14, 1024, 1024, 384, 384, 1, 1, 0),     # 40: = case32 at a 128-B aligned width
+    (64, 14, 14, 384, 384, 1024, 1024, 1, 1, 1),     # 41: = case5 with an aligned input
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
