@@ -644,6 +644,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               o[r4][q] *= fminf(fmaxf(o[r4][q] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+        } else if (EPI == 2 && act == 3) {  // GELU inline (gelu_erf_fast)
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[r4][q] = gelu_erf_fast(o[r4][q]);
         } else if (EPI == 2 && act) {
 #pragma unroll
           for (int r4 = 0; r4 < 4; ++r4)

@@ -644,84 +644,81 @@ __device__ __forceinline__ float* se_hid(const SEParams& p) {
   return p.gate + static_cast<long>(p.n) * p.c_max;
 }
 
-// One warp per output row; each lane reads 8 weights (16 B) and the 8
-// matching pooled values of every sample per step, so a 1152-wide row is 4.5
-// fully independent steps (the scalar version walked C / 32 dependent
-// 2-byte steps per row and was latency-bound at ~65 us per launch).
-__device__ __forceinline__ void ld_f32x8(const float* p, float (&f)[8]) {
-  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
-  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-}
-
-__global__ void __launch_bounds__(256) se_reduce_kernel(SEParams p) {
+// The two SE FCs as one kernel shape: thread = (output row, K slice), eight
+// samples per CTA.  The samples' input rows (pooled / hidden, fp32) are staged
+// once in shared memory and read as broadcasts; each thread streams its own
+// weight row (16-byte loads, L1-resident across the K loop) and keeps 8 sample
+// accumulators, so the inner loop is 8 FMA per 16 B of weights with no warp
+// reduction.  (The warp-per-row version spent more issue slots in its
+// 32-accumulator shuffle reductions than in FMAs: 11-40 us per bs256 launch,
+// ~2 TFMA/s.)  KS K slices per row meet in shared memory in fixed order.
+constexpr int SE_KMAX = 1152;  // widest SE input (OFA-MBv3 w1.2 stage 5)
+template <int KS, bool EXPAND>
+__global__ void __launch_bounds__(256) se_fc_kernel(SEParams p) {
+  __shared__ __align__(16) float xs[SE_NB][SE_KMAX];
+  __shared__ float red[KS > 1 ? KS : 1][SE_NB][256 / KS];
   pdl_wait();
   pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
+  const int K = EXPAND ? mid : C, rows = EXPAND ? C : mid;
+  const float* in = EXPAND ? se_hid(p) : p.pooled;
+  const long in_ld = EXPAND ? p.se_max : p.c_max;
+  const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(EXPAND ? p.w_expand : p.w_reduce);
+  const long w_ld = EXPAND ? p.se_max : p.w_ld;
+  constexpr int RPC = 256 / KS;  // output rows per CTA
+  const int tid = threadIdx.x, rl = tid % RPC, ks = tid / RPC;
+  const int row = blockIdx.y * RPC + rl;
   const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.y * 8 + warp;  // output row
-  if (j >= mid) return;
-  const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.w_reduce) + static_cast<long>(j) * p.w_ld;
-  float* hid = se_hid(p);
+  if (blockIdx.y * RPC >= rows) return;
+  for (int i = tid; i < SE_NB * (K / 4); i += 256) {
+    const int b = i / (K / 4), k4 = i - b * (K / 4);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (b < nb) v = __ldg(reinterpret_cast<const float4*>(in + (n0 + b) * in_ld) + k4);
+    reinterpret_cast<float4*>(xs[b])[k4] = v;
+  }
+  __syncthreads();
   float acc[SE_NB];
 #pragma unroll
   for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
-  for (int c = lane * 8; c < C; c += 256) {
-    float w[8];
-    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wr + c)), w);
+  const int kper = (K / 8 + KS - 1) / KS * 8;
+  const int k0 = ks * kper, k1 = min(K, k0 + kper);
+  if (row < rows) {
+    const __nv_bfloat16* wr = w + row * w_ld;
+    for (int k = k0; k < k1; k += 8) {
+      float wv[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wr + k)), wv);
 #pragma unroll
-    for (int b = 0; b < SE_NB; ++b) {
-      if (b >= nb) break;
-      float x[8];
-      ld_f32x8(p.pooled + static_cast<long>(n0 + b) * p.c_max + c, x);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[b] += w[q] * x[q];
+      for (int b = 0; b < SE_NB; ++b) {
+        const float4 x0 = *reinterpret_cast<const float4*>(&xs[b][k]);
+        const float4 x1 = *reinterpret_cast<const float4*>(&xs[b][k + 4]);
+        acc[b] += wv[0] * x0.x + wv[1] * x0.y + wv[2] * x0.z + wv[3] * x0.w +
+                  wv[4] * x1.x + wv[5] * x1.y + wv[6] * x1.z + wv[7] * x1.w;
+      }
     }
   }
+  if (KS > 1) {
 #pragma unroll
-  for (int b = 0; b < SE_NB; ++b) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-    if (lane == 0 && b < nb) hid[static_cast<long>(n0 + b) * p.se_max + j] = fmaxf(acc[b] + p.b_reduce[j], 0.f);
-  }
-}
-
-__global__ void __launch_bounds__(256) se_expand_kernel(SEParams p) {
-  pdl_wait();
-  pdl_trigger();
-  const OpDims d = load_desc(p.row, nullptr, p.op);
-  const int C = d.cin, mid = desc_ptr(p.row, nullptr, p.op)->aux;
-  const int n0 = blockIdx.x * SE_NB, nb = min(SE_NB, p.n - n0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.y * 8 + warp;  // output channel
-  if (c >= C) return;
-  const __nv_bfloat16* we = static_cast<const __nv_bfloat16*>(p.w_expand) + static_cast<long>(c) * p.se_max;
-  const float* hid = se_hid(p);
-  float acc[SE_NB];
-#pragma unroll
-  for (int b = 0; b < SE_NB; ++b) acc[b] = 0.f;
-  for (int j = lane * 8; j < mid; j += 256) {
-    float w[8];
-    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(we + j)), w);
+    for (int b = 0; b < SE_NB; ++b) red[ks][b][rl] = acc[b];
+    __syncthreads();
+    if (ks != 0) return;
 #pragma unroll
     for (int b = 0; b < SE_NB; ++b) {
-      if (b >= nb) break;
-      float x[8];
-      ld_f32x8(hid + static_cast<long>(n0 + b) * p.se_max + j, x);
+      float t = 0.f;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[b] += w[q] * x[q];
+      for (int z = 0; z < KS; ++z) t += red[z][b][rl];
+      acc[b] = t;
     }
   }
+  if (row >= rows) return;
 #pragma unroll
   for (int b = 0; b < SE_NB; ++b) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-    if (lane == 0 && b < nb)
-      p.gate[static_cast<long>(n0 + b) * p.c_max + c] =
-          fminf(fmaxf(acc[b] + p.b_expand[c] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+    if (b >= nb) break;
+    if (EXPAND)
+      p.gate[static_cast<long>(n0 + b) * p.c_max + row] =
+          fminf(fmaxf(acc[b] + p.b_expand[row] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+    else
+      se_hid(p)[static_cast<long>(n0 + b) * p.se_max + row] = fmaxf(acc[b] + p.b_reduce[row], 0.f);
   }
 }
 
@@ -808,10 +805,12 @@ cudaError_t launch_se(const SEParams& p, cudaStream_t s) {
           : launch_pdl(se_pool_kernel, dim3(p.n, (p.c_max + 63) / 64), dim3(256), 0, s, 1, p);
   if (e != cudaSuccess) return e;
   const int nbk = (p.n + SE_NB - 1) / SE_NB;
-  // one warp per output row
-  e = launch_pdl(se_reduce_kernel, dim3(nbk, (p.se_max + 7) / 8), dim3(256), 0, s, 1, p);
+  if (p.c_max > SE_KMAX || p.se_max > SE_KMAX) return cudaErrorInvalidValue;
+  // reduce: rows = squeeze width (<= 288), K = channels: 4 K slices x 64 rows;
+  // expand: rows = channels, K = squeeze width: 1 slice x 256 rows
+  e = launch_pdl(se_fc_kernel<4, false>, dim3(nbk, (p.se_max + 63) / 64), dim3(256), 0, s, 1, p);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(se_expand_kernel, dim3(nbk, (p.c_max + 7) / 8), dim3(256), 0, s, 1, p);
+  e = launch_pdl(se_fc_kernel<1, true>, dim3(nbk, (p.c_max + 255) / 256), dim3(256), 0, s, 1, p);
   if (e != cudaSuccess) return e;
   return launch_pdl(se_scale_kernel,
                     dim3(grid_for(static_cast<long>(p.n) * p.hw * (p.c_max / 8), 256)), dim3(256),
