@@ -35,6 +35,12 @@
 namespace ssn {
 
 constexpr int DW_CC = 64;        // channels per tile = 32 lanes x bf16x2
+// Narrow layers (max width <= 32, e.g. OFA-MBv3's 24-channel 112-px block):
+// CC = 32-channel boxes, each warp lane-half (16 lanes x bf16x2) owns one
+// pixel, so a warp task covers 2 x 7 outputs.  With 64-channel boxes a
+// 24-channel layer left 20 of 32 lanes idle and staged 80 zero bytes per
+// pixel (0.21 of HBM peak, tools/cudnn_ref.py: cuDNN 2x faster).
+constexpr int DW_CC_NARROW = 32;
 constexpr int DW_QW = 7;         // adjacent outputs per warp task
 constexpr int DW_NCW = 15;       // consumer warps
 constexpr int DW_THREADS = 32 * (DW_NCW + 1);
@@ -137,12 +143,12 @@ __device__ __forceinline__ void dw_store_task(const float2 (&acc)[DW_QW], float2
 
 // One window row of a task: convert its SEG pixels once, accumulate them
 // into output row 0 (filter row wa) and/or output row 1 (filter row wb).
-template <int S, int K, int SEG, bool A, bool B>
+template <int S, int K, int SEG, int LP, bool A, bool B>
 __device__ __forceinline__ void dw_row(const uint32_t* win, const float2* wa, const float2* wb,
                                        float2 (&a)[DW_QW], float2 (&b)[DW_QW]) {
   float2 in[SEG];
 #pragma unroll
-  for (int q = 0; q < SEG; ++q) in[q] = bf2_to_f2(win[q * 32]);
+  for (int q = 0; q < SEG; ++q) in[q] = bf2_to_f2(win[q * LP]);
 #pragma unroll
   for (int ss = 0; ss < K; ++ss) {
     if constexpr (A) {
@@ -158,20 +164,24 @@ __device__ __forceinline__ void dw_row(const uint32_t* win, const float2* wa, co
   }
 }
 
-template <int S, int TW, int TH, int QH, int K>
+template <int S, int TW, int TH, int QH, int K, int CC>
 __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp, const DwRun& r) {
   constexpr int IW = (TW - 1) * S + K;        // staged window width (active k)
   constexpr int SEG = (DW_QW - 1) * S + K;    // window pixels one task row reads
-  constexpr int BPR = TW / DW_QW;             // tasks per tile row
+  constexpr int LP = CC / 2;                  // lanes per pixel (one bf16x2 each)
+  constexpr int HV = 32 / LP;                 // pixels (lane halves) per warp
+  constexpr int BPR = TW / (DW_QW * HV);      // tasks per tile row
+  static_assert(BPR >= 1, "tile narrower than one warp task");
   constexpr int T = TH / QH * BPR;            // tasks per tile
   constexpr int NIR = (QH - 1) * S + K;       // window rows one task reads
   const int lane = threadIdx.x & 31, cw = (threadIdx.x >> 5) - 1;
+  const int lp = lane % LP, half = lane / LP;  // channel pair, output half
   const int off = (p.k_max - K) / 2;          // centre crop of the max kernel
   const __nv_bfloat16* wg = static_cast<const __nv_bfloat16*>(p.w);
   __nv_bfloat16* y = static_cast<__nv_bfloat16*>(p.y);
   const int C = r.C, N = p.n;
   const bool pool = p.pool != nullptr;
-  const float2* wsm = reinterpret_cast<const float2*>(r.wsm) + lane;
+  const float2* wsm = reinterpret_cast<const float2*>(r.wsm) + lane;  // [tap][32 lanes]
   float2 sc = make_float2(1.f, 1.f), sh = make_float2(0.f, 0.f);
   // tile coordinates advance incrementally (no divisions in the loop)
   int ti = static_cast<int>(r.t0 % r.tiles_img);
@@ -185,7 +195,7 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
   int st = 0;
   uint32_t ph = 0;
   for (long t = r.t0; t < r.t1; ++t) {
-    const int c = chunk * DW_CC + 2 * lane;
+    const int c = chunk * CC + 2 * lp;
     const bool cok = c < C;
     if (chunk != cur) {
       // new channel chunk: all consumer warps reload the k x k x 64 weights
@@ -193,7 +203,7 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
       cur = chunk;
       dw_consumer_sync();
       for (int e = threadIdx.x - 32; e < K * K * 32; e += DW_NCW * 32) {
-        const int tap = e >> 5, cp = chunk * DW_CC + 2 * (e & 31);
+        const int tap = e >> 5, cp = chunk * CC + 2 * ((e & 31) % LP);
         const int rr = tap / K, ss = tap - rr * K;
         uint32_t v = 0;
         if (cp < C)
@@ -213,13 +223,13 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
     int j = cw - jt;
     if (j < 0) j += DW_NCW;
     for (; j < T; j += DW_NCW) {
-      const int orow = j / BPR * QH, ocol0 = (j % BPR) * DW_QW;
+      const int orow = j / BPR * QH, ocol0 = (j % BPR) * DW_QW * HV + half * DW_QW;
       float2 acc[QH][DW_QW];
 #pragma unroll
       for (int h = 0; h < QH; ++h)
 #pragma unroll
         for (int q = 0; q < DW_QW; ++q) acc[h][q] = make_float2(0.f, 0.f);
-      const uint32_t* win = tile + (orow * S * IW + ocol0 * S) * 32 + lane;
+      const uint32_t* win = tile + (orow * S * IW + ocol0 * S) * LP + lp;
       // window row ir feeds output row h through filter row ir - h*S.  Three
       // rolled phases (rows feeding only the first output row, both, only
       // the second) keep the filter-row choice branch-free and one converted
@@ -227,18 +237,18 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
       const float2* wrow = wsm;
       if constexpr (QH == 1) {
 #pragma unroll 1
-        for (int ir = 0; ir < K; ++ir, win += IW * 32, wrow += K * 32)
-          dw_row<S, K, SEG, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
+        for (int ir = 0; ir < K; ++ir, win += IW * LP, wrow += K * 32)
+          dw_row<S, K, SEG, LP, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
       } else {
 #pragma unroll 1
-        for (int ir = 0; ir < S; ++ir, win += IW * 32, wrow += K * 32)
-          dw_row<S, K, SEG, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
+        for (int ir = 0; ir < S; ++ir, win += IW * LP, wrow += K * 32)
+          dw_row<S, K, SEG, LP, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
 #pragma unroll 1
-        for (int ir = S; ir < K; ++ir, win += IW * 32, wrow += K * 32)
-          dw_row<S, K, SEG, true, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
+        for (int ir = S; ir < K; ++ir, win += IW * LP, wrow += K * 32)
+          dw_row<S, K, SEG, LP, true, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
 #pragma unroll 1
-        for (int ir = K; ir < NIR; ++ir, win += IW * 32, wrow += K * 32)
-          dw_row<S, K, SEG, false, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
+        for (int ir = K; ir < NIR; ++ir, win += IW * LP, wrow += K * 32)
+          dw_row<S, K, SEG, LP, false, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
       }
       const int ow0 = tw * TW + ocol0;
 #pragma unroll
@@ -256,8 +266,13 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
         }
       }
     }
-    if (pool)
-      *reinterpret_cast<float2*>(r.part + (st * DW_NCW + cw) * DW_CC + 2 * lane) = ps;
+    if (pool) {
+      if (HV == 2) {  // both lane halves summed the same channels
+        ps.x += __shfl_xor_sync(0xffffffffu, ps.x, 16);
+        ps.y += __shfl_xor_sync(0xffffffffu, ps.y, 16);
+      }
+      if (lane < LP) *reinterpret_cast<float2*>(r.part + (st * DW_NCW + cw) * DW_CC + 2 * lane) = ps;
+    }
     // one arrival per warp (count = DW_NCW): per-lane arrivals on one
     // mbarrier serialise in the shared-memory atomic unit.  __syncwarp
     // orders the lanes' part[] stores (and their window reads, already
@@ -285,20 +300,21 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
 
 // Producer warp: one TMA box per tile; when the stage comes back, the
 // consumer warps' SE sums of the tile that used it are added in fixed order.
-template <int S, int TW, int TH>
+template <int S, int TW, int TH, int CC>
 __device__ __forceinline__ void dw_produce(const ConvParams& p, const OpDesc* dp, const DwRun& r,
                                            int k) {
   const int lane = threadIdx.x & 31;
   const CUtensorMap* map = &dp->amap;
   const int pad = k / 2;
   const uint32_t bytes =
-      static_cast<uint32_t>(((TH - 1) * S + k) * ((TW - 1) * S + k) * DW_CC * 2);
+      static_cast<uint32_t>(((TH - 1) * S + k) * ((TW - 1) * S + k) * CC * 2);
   const int nst = p.dw_stages;
   auto flush = [&](long t, int st) {  // SE partial of tile t (its stage st is free)
     const int ti = static_cast<int>(t % r.tiles_img);
     const long rest = t / r.tiles_img;
     const int n = static_cast<int>(rest % p.n);
-    const int c = static_cast<int>(rest / p.n) * DW_CC + 2 * lane;
+    const int c = static_cast<int>(rest / p.n) * CC + 2 * lane;
+    if (2 * lane >= CC) return;
     if (c >= r.C) return;
     float2 s = make_float2(0.f, 0.f);
 #pragma unroll
@@ -323,7 +339,7 @@ __device__ __forceinline__ void dw_produce(const ConvParams& p, const OpDesc* dp
       const int chunk = static_cast<int>(rest / p.n);
       const int th = ti / r.tw_n, tw = ti - th * r.tw_n;
       mbar_arrive_expect_tx(&r.full[st], bytes);
-      tma_load_4d(r.ring + st * p.dw_stage_bytes, map, &r.full[st], chunk * DW_CC,
+      tma_load_4d(r.ring + st * p.dw_stage_bytes, map, &r.full[st], chunk * CC,
                   tw * TW * S - pad, th * TH * S - pad, n);
     }
     if (++st == nst) {
@@ -342,7 +358,7 @@ __device__ __forceinline__ void dw_produce(const ConvParams& p, const OpDesc* dp
   }
 }
 
-template <int S, int TW, int TH, int QH>
+template <int S, int TW, int TH, int QH, int CC = DW_CC>
 __global__ void __launch_bounds__(DW_THREADS, 1) dw_tma_kernel(const __grid_constant__ ConvParams p) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   const int nst = p.dw_stages;
@@ -367,21 +383,21 @@ __global__ void __launch_bounds__(DW_THREADS, 1) dw_tma_kernel(const __grid_cons
   r.tw_n = (p.wo + TW - 1) / TW;
   r.tiles_img = ((p.ho + TH - 1) / TH) * r.tw_n;
   r.C = C;
-  const long total = static_cast<long>((C + DW_CC - 1) / DW_CC) * p.n * r.tiles_img;
+  const long total = static_cast<long>((C + CC - 1) / CC) * p.n * r.tiles_img;
   const long per = (total + gridDim.x - 1) / gridDim.x;
   r.t0 = blockIdx.x * per;
   r.t1 = r.t0 + per < total ? r.t0 + per : total;
   if (r.t0 >= r.t1) return;
   if (threadIdx.x < 32) {
-    dw_produce<S, TW, TH>(p, dp, r, k);
+    dw_produce<S, TW, TH, CC>(p, dp, r, k);
     return;
   }
   if (k == 3)
-    dw_consume<S, TW, TH, QH, 3>(p, dp, r);
+    dw_consume<S, TW, TH, QH, 3, CC>(p, dp, r);
   else if (k == 5)
-    dw_consume<S, TW, TH, QH, 5>(p, dp, r);
+    dw_consume<S, TW, TH, QH, 5, CC>(p, dp, r);
   else
-    dw_consume<S, TW, TH, QH, 7>(p, dp, r);
+    dw_consume<S, TW, TH, QH, 7, CC>(p, dp, r);
 }
 
 // ---------------------------------------------------------------------------
@@ -413,8 +429,13 @@ bool dw_supported(int k_max, int k, int stride) {
 // out: [n][h][w][c] bf16 (c active channels), box {64 ch, (TW-1)*S + k,
 // (7-1)*S + k, 1} for the active k; out-of-bounds (padding, channel tail)
 // is TMA zero fill.
+bool dw_narrow(int c_max, int stride, int wo) {
+  static const bool off = getenv("SSN_DW_NO_NARROW") != nullptr;  // A/B switch
+  return !off && c_max <= DW_CC_NARROW && stride == 1 && wo > 7;
+}
+
 int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int k,
-                    int stride, int wo) {
+                    int stride, int wo, int c_max) {
   EncodeTiledFnD enc = dw_encoder();
   if (!enc || (c & 7) != 0 || !dw_supported(7, k, stride)) return -1;
   const DwShape g = dw_shape(stride, wo);
@@ -422,7 +443,8 @@ int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c,
                         static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(w) * c * 2,
                            static_cast<cuuint64_t>(h) * w * c * 2};
-  cuuint32_t box[4] = {DW_CC, static_cast<cuuint32_t>((g.tw - 1) * stride + k),
+  const cuuint32_t cc = dw_narrow(c_max, stride, wo) ? DW_CC_NARROW : DW_CC;
+  cuuint32_t box[4] = {cc, static_cast<cuuint32_t>((g.tw - 1) * stride + k),
                        static_cast<cuuint32_t>((g.th - 1) * stride + k), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
@@ -442,12 +464,12 @@ static int dw_sm_count() {
   return n;
 }
 
-template <int S, int TW, int TH, int QH>
+template <int S, int TW, int TH, int QH, int CC = DW_CC>
 static cudaError_t launch_dw_inst(const ConvParams& p, size_t smem, int grid, cudaStream_t s) {
   static const cudaError_t attr = cudaFuncSetAttribute(
-      dw_tma_kernel<S, TW, TH, QH>, cudaFuncAttributeMaxDynamicSharedMemorySize, DW_SMEM_MAX);
+      dw_tma_kernel<S, TW, TH, QH, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, DW_SMEM_MAX);
   if (attr != cudaSuccess) return attr;
-  return launch_pdl(dw_tma_kernel<S, TW, TH, QH>, dim3(grid), dim3(DW_THREADS), smem, s, 1, p);
+  return launch_pdl(dw_tma_kernel<S, TW, TH, QH, CC>, dim3(grid), dim3(DW_THREADS), smem, s, 1, p);
 }
 
 // p: the op's max geometry (k_max, cout_max) + graph-baked batch; the active
@@ -457,16 +479,19 @@ cudaError_t launch_dw_bf16(const ConvParams& p0, cudaStream_t s) {
     return cudaErrorInvalidValue;
   ConvParams p = p0;
   const DwShape g = dw_shape(p.stride, p.wo);
+  const bool narrow = dw_narrow(p.cout_max, p.stride, p.wo);
+  const int cc = narrow ? DW_CC_NARROW : DW_CC;
   const int bh = (g.th - 1) * p.stride + p.k_max, bw = (g.tw - 1) * p.stride + p.k_max;
-  p.dw_stage_bytes = (bh * bw * DW_CC * 2 + 127) & ~127;
+  p.dw_stage_bytes = (bh * bw * cc * 2 + 127) & ~127;
   const int per_stage = p.dw_stage_bytes + 16 + DW_NCW * DW_CC * 4;
   p.dw_stages = (DW_SMEM_MAX - DW_WSM_BYTES) / per_stage;
   if (p.dw_stages > DW_MAX_STAGES) p.dw_stages = DW_MAX_STAGES;
   if (p.dw_stages < 2) return cudaErrorInvalidValue;
   const size_t smem = static_cast<size_t>(p.dw_stages) * per_stage + DW_WSM_BYTES;
-  const long tiles = static_cast<long>(cdiv(p.cout_max, DW_CC)) * p.n *
+  const long tiles = static_cast<long>(cdiv(p.cout_max, cc)) * p.n *
                      dw_tiles_per_image(p.stride, p.ho, p.wo);
   const int grid = static_cast<int>(tiles < dw_sm_count() ? tiles : dw_sm_count());
+  if (narrow) return launch_dw_inst<1, 14, 14, 2, DW_CC_NARROW>(p, smem, grid, s);
   if (p.stride == 2) return launch_dw_inst<2, 7, 7, 1>(p, smem, grid, s);
   return g.tw == 14 ? launch_dw_inst<1, 14, 14, 2>(p, smem, grid, s)
                     : launch_dw_inst<1, 7, 7, 1>(p, smem, grid, s);

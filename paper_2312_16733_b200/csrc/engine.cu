@@ -55,7 +55,7 @@ cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
 cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s);
 int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int k,
-                    int stride, int wo);
+                    int stride, int wo, int c_max);
 int dw_tiles_per_image(int stride, int ho, int wo);
 bool dw_supported(int k_max, int k, int stride);
 cudaError_t launch_se(const SEParams& p, cudaStream_t s);
@@ -699,7 +699,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     if (e->bf16 && o.active && o.kind == OP_CONV && o.depthwise) {
       // depthwise input window map (box sized for this subnet's k)
       if (make_dw_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                          o.win, o.cout, o.k, o.stride, o.wout) != 0)
+                          o.win, o.cout, o.k, o.stride, o.wout, o.cout_max) != 0)
         SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (depthwise) failed for op " + std::to_string(oi));
     }
     if (e->bf16 && o.active && (o.kind == OP_CONV || o.kind == OP_LINEAR) && !o.depthwise) {
@@ -1372,7 +1372,7 @@ int ssn_op_dw_bf16(const void* x, int n, int h, int w, int c, const void* wgt, i
     const int pad = k / 2;
     const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
     OpDesc d = plain_desc(c, c, k, pad, scale, shift);
-    if (make_dw_act_map(&d.amap, x, n, h, w, c, k, stride, wo) != 0)
+    if (make_dw_act_map(&d.amap, x, n, h, w, c, k, stride, wo, c_max) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (depthwise) failed");
     ConvParams p{};
     p.x = x;

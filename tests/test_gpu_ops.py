@@ -182,6 +182,10 @@ DW_CASES = [
     (1, 13, 17, 40, 48, 5, 5, 2, 0),      # odd sizes, stride 2, no activation
     (2, 9, 11, 32, 32, 7, 7, 1, 1),       # width not a multiple of 7, single chunk
     (16, 14, 14, 816, 816, 7, 7, 2, 2),   # 14 -> 7 stride 2
+    # narrow layers (c_max <= 32): 32-channel boxes, two pixels per warp
+    (3, 30, 30, 16, 32, 7, 5, 1, 2),      # WeightSlice c < c_max, 5 of 7, h_swish
+    (2, 20, 9, 32, 32, 5, 5, 1, 0),       # odd width > 7 (half-empty second lane half)
+    (1, 15, 28, 8, 24, 3, 3, 1, 1),       # 8 of 24 channels
 ]
 
 

@@ -1,7 +1,7 @@
 # Round profiling bundle (1 GPU): bench lines, launch lists, ncu --set full
 # metrics of the tcgen05 conv kernels.  Outputs under gpurun_out/round/.
 set -u
-O=gpurun_out/round
+O=${O:-gpurun_out/round}
 mkdir -p $O
 timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
@@ -22,3 +22,8 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:conv
   -o /tmp/conv_full python tools/prof_forward.py --steps 1 --warmup 0 --subnets max > /dev/null 2>&1
 ncu -i /tmp/conv_full.ncu-rep --page details --csv > $O/ncu_full_conv_tc_max.csv 2>/dev/null
 ls -la $O
+# summaries (text) next to the raw captures
+python tools/launches.py $O/launches_r50_bs64.csv > $O/launches_r50_bs64_summary.txt 2>&1
+python tools/launches.py $O/launches_mbv3_bs256.csv > $O/launches_mbv3_bs256_summary.txt 2>&1
+python tools/launches.py $O/launches_bert_bs64.csv > $O/launches_bert_bs64_summary.txt 2>&1
+python tools/attribute.py $O/launches_r50_bs64.csv --top 60 > $O/attributed_r50_bs64.txt 2>&1

@@ -2,6 +2,7 @@
 // L2-resident bf16 matrix through a STAGES-deep ring; a consumer warp only
 // waits and releases.  Reports bytes per SM-cycle (profiling aid).
 #include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include "device.cuh"
 using namespace ssn;
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(256, 1) k(const __grid_constant__ CUtensorMap 
       const int s = g % STAGES;
       mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], BYTES);
-      const int row = ((blockIdx.x * 7 + g) * BOX_ROWS) % rows_total;
+      const int row = static_cast<int>((static_cast<long>(blockIdx.x) * (rows_total / 148) + static_cast<long>(g) * BOX_ROWS) % (rows_total - BOX_ROWS));
       tma_load_2d(buf + s * BYTES, &map, &full[s], 0, row);
     }
   } else if (warp == P && lane == 0) {
@@ -56,8 +57,10 @@ void run(CUtensorMap map, int rows_total, long long* d) {
          BOX_ROWS, BOX_ROWS * 128, double(iters) * BOX_ROWS * 128 / mx);
 }
 
-int main() {
-  const int rows = 16384;  // 16384 x 64 bf16 = 2 MB: L2 resident
+int main(int argc, char** argv) {
+  // default 16384 x 64 bf16 = 2 MB (L2 resident, shared by all SMs); argv[1]
+  // = rows, e.g. 1048576 (128 MB: each SM streams its own, mostly distinct data)
+  const int rows = argc > 1 ? atoi(argv[1]) : 16384;
   void* src;
   cudaMalloc(&src, rows * 128);
   cudaMemset(src, 0, rows * 128);
