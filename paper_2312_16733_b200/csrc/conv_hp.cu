@@ -19,8 +19,12 @@
 //    cluster of two CTAs computes two such tiles (consecutive in the
 //    (image, row-block) order) as ONE M = 256 tcgen05.mma.cta_group::2, each
 //    CTA holding its own window and HALF of the weight rows;
-//  * B (the WeightSlice of one (channel block, tap)) streams through a ring
-//    of {64 ch, 1 tap, bn/2 rows} boxes from the max-shape KRSC tensor;
+//  * B (the WeightSlice of one (channel block, filter row)) streams through a
+//    ring of {64 ch, bn/2 rows, 3 taps} boxes of the max-shape KRSC tensor
+//    (a map with the tap dimension outermost, so each tap lands as its own
+//    SW128 K-major block): 24-48 KB per box — one producer thread sustains
+//    about one TMA box per ~460 cycles (tools/ubench/tma_rate.cu), so the
+//    feed rate grows with the box size;
 //  * garbage positions (2 padding columns per row, rows past H) are computed
 //    and dropped by the epilogue: 196/256 of the MMA rows are live at 14 px,
 //    784/896 at 28 px.
@@ -42,7 +46,7 @@ constexpr int HP_EPI_WARPS = 12;
 constexpr int HP_EPI_GROUPS = 3;
 constexpr int HP_STG_LD = 36;
 constexpr int HP_STG_BYTES = HP_EPI_WARPS * 32 * HP_STG_LD * 4;
-constexpr int HP_B_STAGE = HP_BN_MAX / 2 * 128;  // one CTA's half of a (block, tap) B box
+constexpr int HP_TAPS = 3;  // taps (one filter row) per B box
 constexpr int HP_SMEM_MAX = 232448;
 constexpr int HP_NACC = 2;
 
@@ -63,9 +67,10 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
   const int wslot = hp_window_slot(p.w_);
   const uint32_t wbytes = static_cast<uint32_t>(hp_window_bytes(p.w_));
   const int SB = p.h_stages;  // B ring depth
+  const int bstage = HP_TAPS * (p.bn / 2) * 128;  // graph-width filter-row box
   uint8_t* sW = smem;                         // [2] halo windows
-  uint8_t* sB = smem + 2 * wslot;             // [SB] B half-boxes
-  float* stg = reinterpret_cast<float*>(sB + SB * HP_B_STAGE);
+  uint8_t* sB = smem + 2 * wslot;             // [SB] B half-boxes (3 taps each)
+  float* stg = reinterpret_cast<float*>(sB + SB * bstage);
   uint64_t* afull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + HP_STG_BYTES);
   uint64_t* aempty = afull + 2;
   uint64_t* bfull = aempty + 2;
@@ -77,11 +82,10 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
   const int bn = conv_bn_active(p.bn, d.cout, 2);
-  // the subnet row's wmap is sized for conv_tc's tiling of this op; it is
-  // used when its box width happens to match, else the graph's max-width map
-  // (rows past the active width land unused)
-  const bool own_wmap = dp->wrows == bn / 2;
-  const CUtensorMap* wm = own_wmap ? &dp->wmap : &wmap;
+  // the subnet row's hmap has this subnet's tile width; a row without one
+  // uses the graph's max-width map (rows past the active width land unused)
+  const bool own_wmap = dp->hrows == bn / 2;
+  const CUtensorMap* wm = own_wmap ? &dp->hmap : &wmap;
   const int brows = own_wmap ? bn / 2 : p.bn / 2;
   const int nt = (d.cout + bn - 1) / bn;
   const int tpi = (p.h + rt - 1) / rt;           // CTA tiles per image
@@ -150,14 +154,16 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
     }
   } else if (warp == 2 || warp == 3) {
     // ====================================================== weight producers
+    // stage h = (unit, channel block, filter row); warps 2 / 3 alternate
     const int pidx = warp - 2;
     const bool leader = elect_one();
-    const uint32_t btx = static_cast<uint32_t>(brows) * 128 * 2;
+    const uint32_t btx = static_cast<uint32_t>(brows) * 128 * HP_TAPS * 2;
+    const int koff = (p.k_max - 3) / 2;
     int h = 0;
     for (int u = u0; u < units; u += ustep) {
       const int n0 = (u % nt) * bn + static_cast<int>(rank) * (bn / 2);
       for (int cb = 0; cb < ncb; ++cb)
-        for (int tap = 0; tap < 9; ++tap, ++h) {
+        for (int r = 0; r < 3; ++r, ++h) {
           if ((h & 1) != pidx) continue;
           const int s = h % SB;
           mbar_wait(&bempty[s], ((h / SB) & 1) ^ 1);
@@ -165,8 +171,7 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
             if (rank == 0) mbar_arrive(&bfull[s]);
           } else if (leader) {
             if (rank == 0) mbar_arrive_expect_tx(&bfull[s], btx);
-            tma2_load_3d(sB + s * HP_B_STAGE, wm, &bfull[s], cb * 64,
-                         (tap / 3 + (p.k_max - 3) / 2) * p.k_max + tap % 3 + (p.k_max - 3) / 2, n0);
+            tma2_load_3d(sB + s * bstage, wm, &bfull[s], cb * 64, n0, (r + koff) * p.k_max + koff);
           }
           __syncwarp();
         }
@@ -188,17 +193,21 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
           mbar_wait(&afull[w], (g >> 1) & 1);
           const int nks = min(4, (d.cin - cb * 64 + 15) / 16);
           const uint64_t ad = a_base + static_cast<uint64_t>((w * wslot) >> 4);
-          for (int tap = 0; tap < 9; ++tap, ++h) {
-            const int s = h % SB;
-            mbar_wait(&bfull[s], (h / SB) & 1);
+          for (int r = 0; r < 3; ++r, ++h) {
+            const int st = h % SB;
+            mbar_wait(&bfull[st], (h / SB) & 1);
             tc_fence_after();
-            const uint64_t at = ad + static_cast<uint64_t>(((tap / 3) * wp + tap % 3) * 8);
-            const uint64_t bd = b_base + static_cast<uint64_t>((s * HP_B_STAGE) >> 4);
-            for (int kk = 0; kk < nks && !(p.dbg & 2); ++kk)
-              tc2_mma_bf16_elect(acc, at + static_cast<uint64_t>(kk * 2),
-                                 bd + static_cast<uint64_t>(kk * 2), idesc,
-                                 (cb | tap | kk) != 0 ? 1u : 0u);
-            tc2_commit_mc_elect(&bempty[s]);
+            const uint64_t bd0 = b_base + static_cast<uint64_t>((st * bstage) >> 4);
+#pragma unroll
+            for (int sx = 0; sx < 3; ++sx) {
+              const uint64_t at = ad + static_cast<uint64_t>((r * wp + sx) * 8);
+              const uint64_t bd = bd0 + static_cast<uint64_t>((sx * brows * 128) >> 4);
+              for (int kk = 0; kk < nks && !(p.dbg & 2); ++kk)
+                tc2_mma_bf16_elect(acc, at + static_cast<uint64_t>(kk * 2),
+                                   bd + static_cast<uint64_t>(kk * 2), idesc,
+                                   (cb | r | sx | kk) != 0 ? 1u : 0u);
+            }
+            tc2_commit_mc_elect(&bempty[st]);
             __syncwarp();
           }
           tc2_commit_mc_elect(&aempty[w]);  // window w free once its 9 taps retire
@@ -306,20 +315,45 @@ static EncodeTiledFnP hp_encoder() {
   return fn;
 }
 
-static int hp_b_stages(int w) {
+// N tile of a pair: the active width in <= 256-wide, 32-aligned tiles
+int hp_choose_bn(int cout_max) {
+  const int nt = (cout_max + HP_BN_MAX - 1) / HP_BN_MAX;
+  const int b = (cout_max + nt - 1) / nt;
+  return (b + 31) / 32 * 32;
+}
+
+static int hp_b_stages(int w, int bn) {
   const long avail = HP_SMEM_MAX - 1024 - 2L * hp_window_slot(w) - HP_STG_BYTES - 256;
-  const long st = avail / HP_B_STAGE;
+  const long st = avail / (static_cast<long>(HP_TAPS) * (bn / 2) * 128);
   return static_cast<int>(st > 8 ? 8 : st);
+}
+
+// B operand of conv_hp: the max-shape KRSC tensor [cout][taps][cin_store]
+// viewed as {cin_store, cout, taps} (tap dimension outermost) with boxes
+// {64 ch, rows, 3 taps}: one filter row of one 64-channel block, each tap a
+// contiguous [rows][128 B] SW128 K-major block.
+int make_hp_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int rows) {
+  EncodeTiledFnP enc = hp_encoder();
+  if (!enc) return -1;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin_store), static_cast<cuuint64_t>(cout),
+                        static_cast<cuuint64_t>(taps)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(taps) * cin_store * 2,
+                           static_cast<cuuint64_t>(cin_store) * 2};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), HP_TAPS};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
 }
 
 // Wide stride-1 3x3 convs whose max width exceeds the resident-weight halo
 // kernel (conv_halo: cout <= 128).  k_max 3 only (OFA-ResNet50).  Measured
-// (ncu device time, tools/microbench_conv.py, profiles/round2/README.md): at
-// 14 px it beats conv_tc's im2col path (360 ch bs64 46 vs 53 us, bs256 141 vs
-// 172 us); at 28 px it loses (176 ch 46 vs 38 us: 87.5% live rows and a
-// ragged last wave of pair tiles), so the graph uses it up to 20 px only
+// against conv_tc's im2col path (ncu device time, tools/microbench_conv.py,
+// profiles/round2/README.md): 360 ch at 14 px bs64 38 vs 53 us, bs256 113 vs
+// 172 us; 176 ch at 28 px 34.5 vs 38 us.  The graph uses it up to 30 px
 // (SSN_HP_MAX_W overrides for experiments; the operator API, graph = false,
-// takes any width so the parity tests cover the 28-px geometry).
+// takes any width so the parity tests cover other geometries).
 bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max, bool graph) {
   static const bool off = [] {
     const char* e = getenv("SSN_NO_HP");  // A/B switch for profiling
@@ -327,11 +361,11 @@ bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max,
   }();
   static const int max_w = [] {
     const char* e = getenv("SSN_HP_MAX_W");
-    return e ? atoi(e) : 20;
+    return e ? atoi(e) : 30;
   }();
   if (off || stride != 1 || k_max != 3 || h < 8 || w < 12 || w > 62 || (graph && w > max_w)) return false;
   if (cout_max <= 128 || (cout_max & 7) != 0 || (cin_max & 7) != 0) return false;
-  return hp_b_stages(w) >= 3;
+  return hp_b_stages(w, hp_choose_bn(cout_max)) >= 2;
 }
 
 // A operand: [n][h][w][cin_a] NHWC bf16, box {64 ch, Wp, R, 1}, 128-byte
@@ -352,13 +386,6 @@ int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int ci
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
 }
 
-// N tile of a pair: the active width in <= 256-wide, 32-aligned tiles
-int hp_choose_bn(int cout_max) {
-  const int nt = (cout_max + HP_BN_MAX - 1) / HP_BN_MAX;
-  const int b = (cout_max + nt - 1) / nt;
-  return (b + 31) / 32 * 32;
-}
-
 static int hp_sm_count() {
   static int n = 0;
   if (!n) {
@@ -376,16 +403,17 @@ cudaError_t init_conv_hp() {
 }
 
 // p: the op's max geometry + graph-baked batch, p.bn = hp_choose_bn(cout_max);
-// wmap: max-width weight map with bn / 2 rows per box.
+// wmap: make_hp_weight_map at the graph width (bn / 2 rows per box).
 cudaError_t launch_conv_hp(ConvParams p, const CUtensorMap& wmap, cudaStream_t s) {
   static const int dbg = [] {
     const char* e = getenv("SSN_TC_DEBUG");
     return e ? atoi(e) : 0;
   }();
   p.dbg = dbg;
-  p.h_stages = hp_b_stages(p.w_);
-  if (p.h_stages < 3 || p.ho != p.h || p.wo != p.w_) return cudaErrorInvalidValue;
-  const long smem = 1024 + 2L * hp_window_slot(p.w_) + static_cast<long>(p.h_stages) * HP_B_STAGE +
+  p.h_stages = hp_b_stages(p.w_, p.bn);
+  if (p.h_stages < 2 || p.ho != p.h || p.wo != p.w_) return cudaErrorInvalidValue;
+  const long smem = 1024 + 2L * hp_window_slot(p.w_) +
+                    static_cast<long>(p.h_stages) * HP_TAPS * (p.bn / 2) * 128 +
                     HP_STG_BYTES + (4 + 2 * p.h_stages + 2 * HP_NACC) * 8 + 16;
   const HaloGeom g = halo_geom(p.w_, 3);
   const long pairs = (static_cast<long>(p.n) * ((p.h + g.rt - 1) / g.rt) + 1) / 2;

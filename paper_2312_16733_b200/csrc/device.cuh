@@ -35,6 +35,10 @@ struct alignas(64) OpDesc {
   // the active tile width / CTAs per tile; 0 = use the graph's map)
   CUtensorMap wmap;
   int wrows;
+  // conv_hp (shifted-window pair kernel): B of one FILTER ROW (3 taps) per
+  // box {64 ch, hrows, 3 taps} at this subnet's tile width (0 = graph map)
+  CUtensorMap hmap;
+  int hrows;
 };
 
 // Active N-tile width of a tcgen05 conv: the graph-baked width bn_g (sized

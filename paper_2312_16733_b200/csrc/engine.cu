@@ -47,6 +47,7 @@ cudaError_t init_conv_hp();
 bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max, bool graph);
 int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin);
 int hp_choose_bn(int cout_max);
+int make_hp_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int rows);
 cudaError_t launch_conv_hp(ConvParams p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t launch_input(const InputParams& p, cudaStream_t s);
 cudaError_t launch_stem_conv(const StemParams& p, cudaStream_t s);
@@ -439,7 +440,7 @@ static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cud
       } else if (bf && use_hp(e, o, batch)) {
         p.bn = hp_choose_bn(o.cout_max);
         CUtensorMap wmap{};
-        if (make_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn / 2) != 0)
+        if (make_hp_weight_map(&wmap, p.w, t.cin_store, o.k_max * o.k_max, t.cout, p.bn / 2) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed for op " + std::to_string(oi));
         CUDA_TRY(launch_conv_hp(p, wmap, s));
       } else if (bf && !o.depthwise) {
@@ -730,10 +731,16 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
         // 14-px 3x3 convs): its 4-D window map rides in the unused rmap slot
         // (B comes from the graph's max-width map), so the same subnet row
         // also serves the small-batch graphs' conv_tc
-        if (use_hp(e, o, e->desc.max_batch) &&
-            make_hp_act_map(&dsc.rmap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                            o.win, o.cin) != 0)
-          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (hp) failed for op " + std::to_string(oi));
+        if (use_hp(e, o, e->desc.max_batch)) {
+          const TensorSpec& t = e->net.tensors[o.tensor];
+          const int hb = conv_bn_active(hp_choose_bn(o.cout_max), o.cout, 2);
+          if (make_hp_act_map(&dsc.rmap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
+                              o.win, o.cin) != 0 ||
+              make_hp_weight_map(&dsc.hmap, e->d_w + t.w_off, t.cin_store, o.k_max * o.k_max,
+                                 t.cout, hb / 2) != 0)
+            SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (hp) failed for op " + std::to_string(oi));
+          dsc.hrows = hb / 2;
+        }
         // residual source for conv_tc's TMA residual ring
         if (res_ptr[oi] && (o.cout & 7) == 0 &&
             make_res_map(&dsc.rmap, res_ptr[oi],
@@ -1336,12 +1343,12 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
       const int bn_a = conv_bn_active(p.bn, cout, 2);
       OpDesc d2 = d;
       if (make_hp_act_map(&d2.rmap, x, n, h, w, cin) != 0 ||
-          make_weight_map(&d2.wmap, wgt, cin_max, k * k, cout_max, bn_a / 2) != 0)
+          make_hp_weight_map(&d2.hmap, wgt, cin_max, k * k, cout_max, bn_a / 2) != 0)
         SSN_THROW(SSN_E_CUDA, "cuTensorMapEncode (hp) failed");
-      d2.wrows = bn_a / 2;
+      d2.hrows = bn_a / 2;
       p.fixed = op_desc_scratch(d2, s);
       CUtensorMap wmap{};
-      if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn / 2) != 0)
+      if (make_hp_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.bn / 2) != 0)
         SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
       CUDA_TRY(launch_conv_hp(p, wmap, s));
       return;
