@@ -28,8 +28,8 @@
 //  * garbage positions (2 padding columns per row, rows past H) are computed
 //    and dropped by the epilogue: 196/256 of the MMA rows are live at 14 px,
 //    784/896 at 28 px.
-// Warp roles (512 threads): warp 0 window producer, warp 1 MMA issuer (CTA 0
-// of the pair), warps 2-3 weight producers (alternate stages), warps 4-15 the
+// Warp roles (384 threads): warp 0 window producer, warp 1 MMA issuer (CTA 0
+// of the pair), warps 2-3 weight producers (alternate stages), warps 4-11 the
 // epilogue (TMEM -> padded smem transpose -> SubnetNorm + activation on
 // coalesced 64-byte row segments), as conv_tc.  Two TMEM accumulators.
 #include <cstdio>
@@ -40,10 +40,13 @@
 namespace ssn {
 
 constexpr int HP_BN_MAX = 256;
-constexpr int HP_THREADS = 512;
+// 8 epilogue warps (2 groups of 4 TMEM lane quarters): a pair unit is
+// ~20k MMA cycles, its epilogue a few thousand, and the 18 KB of staging a
+// third group would need buys a 4th weight stage instead
 constexpr int HP_EPI_WARP0 = 4;
-constexpr int HP_EPI_WARPS = 12;
-constexpr int HP_EPI_GROUPS = 3;
+constexpr int HP_EPI_WARPS = 8;
+constexpr int HP_EPI_GROUPS = 2;
+constexpr int HP_THREADS = (HP_EPI_WARP0 + HP_EPI_WARPS) * 32;
 constexpr int HP_STG_LD = 36;
 constexpr int HP_STG_BYTES = HP_EPI_WARPS * 32 * HP_STG_LD * 4;
 constexpr int HP_TAPS = 3;  // taps (one filter row) per B box

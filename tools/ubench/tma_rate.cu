@@ -92,5 +92,8 @@ int main(int argc, char** argv) {
   run<6, 256, 2>(mk(256), rows, d);
   run<8, 128, 4>(mk(128), rows, d);
   run<8, 256, 4>(mk(256), rows, d);
+  run<4, 256, 2>(mk(256), rows, d);
+  run<3, 256, 2>(mk(256), rows, d);
+  run<4, 256, 1>(mk(256), rows, d);
   return 0;
 }
