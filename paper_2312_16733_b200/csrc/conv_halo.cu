@@ -85,6 +85,11 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   uint64_t* tempty = tfull + 4;    // [4]
   uint64_t* bfull = tempty + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  // SubnetNorm scale / shift of this op (cout <= 128), staged once: the
+  // row-per-lane epilogue reads all columns per lane, and per-column global
+  // loads issued right before their FMAs serialised an L1/L2 round trip per
+  // 8 columns (ncu: the epilogue's FFMAs were the top stall site)
+  float* sn = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));  // [2][128]
 
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through shfl: the compiler then knows it is warp-uniform, so
@@ -214,6 +219,11 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     // ============================================================ epilogue
     // Lane L of warp w drains TMEM row 32*(w%4) + L = one padded output
     // position; positions in the padding columns / past H are dropped.
+    for (int i = tid - 32; i < 128; i += HL_EPI_WARPS * 32) {  // static: before the PDL wait
+      sn[i] = (d.scale && i < d.cout) ? __ldg(d.scale + i) : 1.f;
+      sn[128 + i] = (d.shift && i < d.cout) ? __ldg(d.shift + i) : 0.f;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(HL_EPI_WARPS * 32) : "memory");
     pdl_wait();  // the residual is the predecessors' output
     const int quarter = warp & 3;
     const int group = (warp - 1) >> 2;
@@ -255,23 +265,15 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
           const int col = c * 32 + 8 * j;
           if (col >= d.cout) break;
           float sc[8], sh[8];
-          if (d.scale) {
-            const float4 s0 = __ldg(reinterpret_cast<const float4*>(d.scale + col));
-            const float4 s1 = __ldg(reinterpret_cast<const float4*>(d.scale + col + 4));
+          {
+            const float4 s0 = *reinterpret_cast<const float4*>(sn + col);
+            const float4 s1 = *reinterpret_cast<const float4*>(sn + col + 4);
+            const float4 h0 = *reinterpret_cast<const float4*>(sn + 128 + col);
+            const float4 h1 = *reinterpret_cast<const float4*>(sn + 128 + col + 4);
             sc[0] = s0.x; sc[1] = s0.y; sc[2] = s0.z; sc[3] = s0.w;
             sc[4] = s1.x; sc[5] = s1.y; sc[6] = s1.z; sc[7] = s1.w;
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sc[q] = 1.f;
-          }
-          if (d.shift) {
-            const float4 h0 = __ldg(reinterpret_cast<const float4*>(d.shift + col));
-            const float4 h1 = __ldg(reinterpret_cast<const float4*>(d.shift + col + 4));
             sh[0] = h0.x; sh[1] = h0.y; sh[2] = h0.z; sh[3] = h0.w;
             sh[4] = h1.x; sh[5] = h1.y; sh[6] = h1.z; sh[7] = h1.w;
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sh[q] = 0.f;
           }
           float o[8];
 #pragma unroll
@@ -368,7 +370,7 @@ static void halo_sizes(int w, int k_max, int cin_max, int cout_max, long* b_byte
 static int halo_stages(int w, int k_max, int cin_max, int cout_max) {
   long bb, as;
   halo_sizes(w, k_max, cin_max, cout_max, &bb, &as);
-  const long avail = HL_SMEM_MAX - 1024 - ((bb + 1023) & ~1023L) - 256;
+  const long avail = HL_SMEM_MAX - 1024 - ((bb + 1023) & ~1023L) - 256 - 2 * 128 * 4;
   const long st = avail / as;
   return static_cast<int>(st > 6 ? 6 : st);
 }
@@ -458,7 +460,8 @@ cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int t
     return cudaErrorInvalidValue;
   long bb, as;
   halo_sizes(p.w_, p.k_max, p.cin_max, p.cout_max, &bb, &as);
-  const long smem = 1024 + ((bb + 1023) & ~1023L) + p.h_stages * as + (2 * p.h_stages + 9) * 8 + 16;
+  const long smem = 1024 + ((bb + 1023) & ~1023L) + p.h_stages * as + (2 * p.h_stages + 9) * 8 + 16 +
+                    2 * 128 * 4 + 32;
   const HaloGeom g = halo_geom(p.w_, p.k_max);
   const long tiles = static_cast<long>(p.n) * ((p.h + g.rt - 1) / g.rt);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
