@@ -110,12 +110,12 @@ __device__ __forceinline__ void dw_consumer_sync() {
 // on the packed bf16 pair (rounding commutes with max(., 0)); the pool adds
 // with a packed FMA.  FULL: all 7 outputs inside the image (no per-pixel
 // bounds test).
-template <int ACT, bool FULL>
-__device__ __forceinline__ void dw_epilogue(const float2 (&acc)[DW_QW], float2 sc, float2 sh,
+template <int ACT, bool FULL, int QW>
+__device__ __forceinline__ void dw_epilogue(const float2 (&acc)[QW], float2 sc, float2 sh,
                                             __nv_bfloat16* yr, int C, int nvalid, bool pool,
                                             float2& ps) {
 #pragma unroll
-  for (int q = 0; q < DW_QW; ++q) {
+  for (int q = 0; q < QW; ++q) {
     if (FULL || q < nvalid) {
       const float2 v = dw_ffma2(acc[q], sc, sh);
       uint32_t u;
@@ -131,21 +131,21 @@ __device__ __forceinline__ void dw_epilogue(const float2 (&acc)[DW_QW], float2 s
   }
 }
 
-template <int ACT>
-__device__ __forceinline__ void dw_store_task(const float2 (&acc)[DW_QW], float2 sc, float2 sh,
+template <int ACT, int QW>
+__device__ __forceinline__ void dw_store_task(const float2 (&acc)[QW], float2 sc, float2 sh,
                                               __nv_bfloat16* yr, int C, int nvalid, bool pool,
                                               float2& ps) {
-  if (nvalid >= DW_QW)
-    dw_epilogue<ACT, true>(acc, sc, sh, yr, C, nvalid, pool, ps);
+  if (nvalid >= QW)
+    dw_epilogue<ACT, true, QW>(acc, sc, sh, yr, C, nvalid, pool, ps);
   else
-    dw_epilogue<ACT, false>(acc, sc, sh, yr, C, nvalid, pool, ps);
+    dw_epilogue<ACT, false, QW>(acc, sc, sh, yr, C, nvalid, pool, ps);
 }
 
 // One window row of a task: convert its SEG pixels once, accumulate them
 // into output row 0 (filter row wa) and/or output row 1 (filter row wb).
-template <int S, int K, int SEG, int LP, bool A, bool B>
+template <int S, int K, int SEG, int LP, int QW, bool A, bool B>
 __device__ __forceinline__ void dw_row(const uint32_t* win, const float2* wa, const float2* wb,
-                                       float2 (&a)[DW_QW], float2 (&b)[DW_QW]) {
+                                       float2 (&a)[QW], float2 (&b)[QW]) {
   float2 in[SEG];
 #pragma unroll
   for (int q = 0; q < SEG; ++q) in[q] = bf2_to_f2(win[q * LP]);
@@ -154,23 +154,23 @@ __device__ __forceinline__ void dw_row(const uint32_t* win, const float2* wa, co
     if constexpr (A) {
       const float2 wv = wa[ss * 32];
 #pragma unroll
-      for (int q = 0; q < DW_QW; ++q) a[q] = dw_ffma2(in[q * S + ss], wv, a[q]);
+      for (int q = 0; q < QW; ++q) a[q] = dw_ffma2(in[q * S + ss], wv, a[q]);
     }
     if constexpr (B) {
       const float2 wv = wb[ss * 32];
 #pragma unroll
-      for (int q = 0; q < DW_QW; ++q) b[q] = dw_ffma2(in[q * S + ss], wv, b[q]);
+      for (int q = 0; q < QW; ++q) b[q] = dw_ffma2(in[q * S + ss], wv, b[q]);
     }
   }
 }
 
-template <int S, int TW, int TH, int QH, int K, int CC>
+template <int S, int TW, int TH, int QH, int QW, int K, int CC>
 __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp, const DwRun& r) {
   constexpr int IW = (TW - 1) * S + K;        // staged window width (active k)
-  constexpr int SEG = (DW_QW - 1) * S + K;    // window pixels one task row reads
+  constexpr int SEG = (QW - 1) * S + K;       // window pixels one task row reads
   constexpr int LP = CC / 2;                  // lanes per pixel (one bf16x2 each)
   constexpr int HV = 32 / LP;                 // pixels (lane halves) per warp
-  constexpr int BPR = TW / (DW_QW * HV);      // tasks per tile row
+  constexpr int BPR = TW / (QW * HV);         // tasks per tile row
   static_assert(BPR >= 1, "tile narrower than one warp task");
   constexpr int T = TH / QH * BPR;            // tasks per tile
   constexpr int NIR = (QH - 1) * S + K;       // window rows one task reads
@@ -223,12 +223,12 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
     int j = cw - jt;
     if (j < 0) j += DW_NCW;
     for (; j < T; j += DW_NCW) {
-      const int orow = j / BPR * QH, ocol0 = (j % BPR) * DW_QW * HV + half * DW_QW;
-      float2 acc[QH][DW_QW];
+      const int orow = j / BPR * QH, ocol0 = (j % BPR) * QW * HV + half * QW;
+      float2 acc[QH][QW];
 #pragma unroll
       for (int h = 0; h < QH; ++h)
 #pragma unroll
-        for (int q = 0; q < DW_QW; ++q) acc[h][q] = make_float2(0.f, 0.f);
+        for (int q = 0; q < QW; ++q) acc[h][q] = make_float2(0.f, 0.f);
       const uint32_t* win = tile + (orow * S * IW + ocol0 * S) * LP + lp;
       // window row ir feeds output row h through filter row ir - h*S.  Three
       // rolled phases (rows feeding only the first output row, both, only
@@ -238,17 +238,17 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
       if constexpr (QH == 1) {
 #pragma unroll 1
         for (int ir = 0; ir < K; ++ir, win += IW * LP, wrow += K * 32)
-          dw_row<S, K, SEG, LP, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
+          dw_row<S, K, SEG, LP, QW, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
       } else {
 #pragma unroll 1
         for (int ir = 0; ir < S; ++ir, win += IW * LP, wrow += K * 32)
-          dw_row<S, K, SEG, LP, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
+          dw_row<S, K, SEG, LP, QW, true, false>(win, wrow, wrow, acc[0], acc[QH - 1]);
 #pragma unroll 1
         for (int ir = S; ir < K; ++ir, win += IW * LP, wrow += K * 32)
-          dw_row<S, K, SEG, LP, true, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
+          dw_row<S, K, SEG, LP, QW, true, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
 #pragma unroll 1
         for (int ir = K; ir < NIR; ++ir, win += IW * LP, wrow += K * 32)
-          dw_row<S, K, SEG, LP, false, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
+          dw_row<S, K, SEG, LP, QW, false, true>(win, wrow, wrow - S * K * 32, acc[0], acc[QH - 1]);
       }
       const int ow0 = tw * TW + ocol0;
 #pragma unroll
@@ -258,11 +258,11 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
           __nv_bfloat16* yr = y + (static_cast<long>(n * p.ho + oh) * p.wo + ow0) * C + c;
           const int nvalid = p.wo - ow0;
           if (p.act == 1)
-            dw_store_task<1>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
+            dw_store_task<1, QW>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
           else if (p.act == 2)
-            dw_store_task<2>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
+            dw_store_task<2, QW>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
           else
-            dw_store_task<0>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
+            dw_store_task<0, QW>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
         }
       }
     }
@@ -358,7 +358,7 @@ __device__ __forceinline__ void dw_produce(const ConvParams& p, const OpDesc* dp
   }
 }
 
-template <int S, int TW, int TH, int QH, int CC = DW_CC>
+template <int S, int TW, int TH, int QH, int CC = DW_CC, int QW = DW_QW>
 __global__ void __launch_bounds__(DW_THREADS, 1) dw_tma_kernel(const __grid_constant__ ConvParams p) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   const int nst = p.dw_stages;
@@ -392,12 +392,12 @@ __global__ void __launch_bounds__(DW_THREADS, 1) dw_tma_kernel(const __grid_cons
     dw_produce<S, TW, TH, CC>(p, dp, r, k);
     return;
   }
-  if (k == 3)
-    dw_consume<S, TW, TH, QH, 3, CC>(p, dp, r);
+  if (k == 3)  // HBM-bound: 7-wide tasks (14-wide measured 5% slower at k = 3)
+    dw_consume<S, TW, TH, QH, DW_QW, 3, CC>(p, dp, r);
   else if (k == 5)
-    dw_consume<S, TW, TH, QH, 5, CC>(p, dp, r);
+    dw_consume<S, TW, TH, QH, QW, 5, CC>(p, dp, r);
   else
-    dw_consume<S, TW, TH, QH, 7, CC>(p, dp, r);
+    dw_consume<S, TW, TH, QH, QW, 7, CC>(p, dp, r);
 }
 
 // ---------------------------------------------------------------------------
@@ -447,9 +447,17 @@ int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c,
   cuuint32_t box[4] = {cc, static_cast<cuuint32_t>((g.tw - 1) * stride + k),
                        static_cast<cuuint32_t>((g.th - 1) * stride + k), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
+  static const int promo = [] {  // A/B switch: L2 promotion of the window rows
+    const char* e = getenv("SSN_DW_L2PROMO");
+    return e ? atoi(e) : 256;
+  }();
+  const CUtensorMapL2promotion pr = promo == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r);
 }
 
@@ -464,12 +472,12 @@ static int dw_sm_count() {
   return n;
 }
 
-template <int S, int TW, int TH, int QH, int CC = DW_CC>
+template <int S, int TW, int TH, int QH, int CC = DW_CC, int QW = DW_QW>
 static cudaError_t launch_dw_inst(const ConvParams& p, size_t smem, int grid, cudaStream_t s) {
   static const cudaError_t attr = cudaFuncSetAttribute(
-      dw_tma_kernel<S, TW, TH, QH, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, DW_SMEM_MAX);
+      dw_tma_kernel<S, TW, TH, QH, CC, QW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DW_SMEM_MAX);
   if (attr != cudaSuccess) return attr;
-  return launch_pdl(dw_tma_kernel<S, TW, TH, QH, CC>, dim3(grid), dim3(DW_THREADS), smem, s, 1, p);
+  return launch_pdl(dw_tma_kernel<S, TW, TH, QH, CC, QW>, dim3(grid), dim3(DW_THREADS), smem, s, 1, p);
 }
 
 // p: the op's max geometry (k_max, cout_max) + graph-baked batch; the active
@@ -493,6 +501,12 @@ cudaError_t launch_dw_bf16(const ConvParams& p0, cudaStream_t s) {
   const int grid = static_cast<int>(tiles < dw_sm_count() ? tiles : dw_sm_count());
   if (narrow) return launch_dw_inst<1, 14, 14, 2, DW_CC_NARROW>(p, smem, grid, s);
   if (p.stride == 2) return launch_dw_inst<2, 7, 7, 1>(p, smem, grid, s);
+  // 14-wide warp tasks for k = 5 / 7 (each converted window pixel feeds up
+  // to 14 outputs x 2 rows): FFMA2 share of the inner loop 63% -> 73% for the
+  // FMA-pipe-bound layers (56 px k7 420 -> 399 us at bs256); k = 3 keeps
+  // 7-wide tasks; SSN_DW_QW7 = 7-wide everywhere (A/B switch)
+  static const bool qw7 = getenv("SSN_DW_QW7") != nullptr;
+  if (g.tw == 14 && !qw7) return launch_dw_inst<1, 14, 14, 2, DW_CC, 14>(p, smem, grid, s);
   return g.tw == 14 ? launch_dw_inst<1, 14, 14, 2>(p, smem, grid, s)
                     : launch_dw_inst<1, 7, 7, 1>(p, smem, grid, s);
 }
