@@ -284,18 +284,44 @@ def run_ours(args, rank, world, local_rank):
     imgs_per_rank = args.steps * len(SUBNETS) * B
     value = world * imgs_per_rank / (ms / 1000.0)
 
-    # ---- e2e through the C-ABI with pinned host buffers
+    # ---- e2e through the C-ABI with pinned host buffers, run as a serving
+    # loop: step i+1 (its H2D images, three forwards, its D2H logits) is
+    # enqueued before the host reads step i's logits, so the copy engine works
+    # under the previous step's kernels instead of after a drained stream.
+    # Every step's H2D and D2H and the host read of every step's logits are
+    # inside the timed region; two logit buffer sets alternate by step parity.
     xh = [torch.randint(0, 256, (B, args.image, args.image, 3), dtype=torch.uint8).pin_memory()
           for _ in range(2)]
-    lh = [torch.empty((B, 1000), dtype=torch.float32).pin_memory() for _ in SUBNETS]
+    lh = [[torch.empty((B, 1000), dtype=torch.float32).pin_memory() for _ in SUBNETS]
+          for _ in range(2)]
+    pend = []
+
+    def host_read():
+        ev, bufs = pend.pop(0)
+        ev.synchronize()
+        return float(bufs[-1][0, 0])
 
     def e2e_step(i):
-        step(i, (xh, lh))
-        stream.synchronize()  # the step's logits are read on the host
-        _ = float(lh[-1][0, 0])
+        step(i, (xh, lh[i % 2]))
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        pend.append((ev, lh[i % 2]))
+        if len(pend) > 1:
+            host_read()  # step i-1's logits, while step i runs
 
-    _, e2e_ms = timed_region(e2e_step, args.steps, args.warmup, CudaTimer(torch, stream),
-                             sync=torch.cuda.synchronize)
+    def e2e_sync():
+        while pend:
+            host_read()
+        torch.cuda.synchronize()
+
+    class DrainTimer(CudaTimer):  # the last step's host read ends the region
+        def stop(self):
+            while pend:
+                host_read()
+            return super().stop()
+
+    _, e2e_ms = timed_region(e2e_step, args.steps, args.warmup, DrainTimer(torch, stream),
+                             sync=e2e_sync)
     e2e_value = world * imgs_per_rank / (e2e_ms / 1000.0)
 
     # ---- config 4 at every N: SlackFit dispatch across the N replicas
@@ -335,6 +361,8 @@ def run_ours(args, rank, world, local_rank):
                 "default SubnetNorm rows)",
         "config": workload_config(args, world),
         "e2e": {"value": e2e_value, "unit": "images/s",
+                "mode": "serving loop: step i+1 enqueued (H2D + forwards + D2H) before the host "
+                        "reads step i's logits; every copy and read inside the timed region",
                 "h2d_bytes_per_step": len(SUBNETS) * B * img_bytes,
                 "d2h_bytes_per_step": len(SUBNETS) * B * 1000 * 4},
         "gpu_launches": launches,
