@@ -598,7 +598,7 @@ def driver_roofline(eng, desc, cfgs, B, peaks, ssn, step_ms):
     head = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["tc"],
             "unit": "TFLOP/s", "frac": round(achieved / peaks["tc"], 4), "traffic": traffic,
             "algorithmic_bytes_per_launch": round(conv_b / max(n_conv, 1)),
-            "kernel": "conv_tc_kernel / conv_halo_kernel (tcgen05 WeightSlice implicit GEMM), "
+            "kernel": "conv_tc_kernel / conv_halo_kernel / conv_hp_kernel (tcgen05 WeightSlice implicit GEMM), "
                       f"all conv launches of the {{{','.join(SUBNETS)}}} sweep at bs{B}",
             "peak_source": f"{peaks['src']} bf16_tflops (burst)",
             "conv_us_per_step": round(conv_us, 1),
