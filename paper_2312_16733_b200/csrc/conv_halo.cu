@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
       const int oh = (t - img * tpi) * rt + oh_l;
       const bool ok = p_row < rt * wp && ow < p.wo && oh < p.ho;
       const size_t m = (static_cast<size_t>(img) * p.ho + oh) * p.wo + ow;
-      const size_t rowoff = m * d.cout;
+      const size_t rowoff = m * d.ldo;
       HL_WAIT(w_wait, &tfull[a], static_cast<uint32_t>(i / nacc) & 1);
       tc_fence_after();
       for (int c = 0; c < nch; ++c) {
@@ -392,14 +392,14 @@ bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_ma
 
 // A operand: [n][h][w][cin_a] NHWC bf16, box {32 ch, Wp, R, 1} with 64-byte
 // swizzle: one halo window of one 32-channel block as 64-B pixel rows.
-int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k) {
+int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld, int k) {
   EncodeTiledFnH enc = tiled_encoder();
   if (!enc) return -1;
   const HaloGeom g = halo_geom(w, k);
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
                         static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(w) * cin * 2,
-                           static_cast<cuuint64_t>(h) * w * cin * 2};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(w) * ld * 2,
+                           static_cast<cuuint64_t>(h) * w * ld * 2};
   cuuint32_t box[4] = {HL_CB, static_cast<cuuint32_t>(g.wp), static_cast<cuuint32_t>(g.r), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,

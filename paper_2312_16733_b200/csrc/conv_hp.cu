@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
             pk.z = pack_bf16x2(o[4], o[5]);
             pk.w = pack_bf16x2(o[6], o[7]);
             const size_t m = (static_cast<size_t>(img) * p.ho + oh) * p.wo + cc;
-            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + m * d.cout + col) = pk;
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + m * d.ldo + col) = pk;
           }
         }
         __syncwarp();  // staging tile is rewritten by the next chunk
@@ -373,14 +373,14 @@ bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max,
 
 // A operand: [n][h][w][cin_a] NHWC bf16, box {64 ch, Wp, R, 1}, 128-byte
 // swizzle: one halo window of one 64-channel block as 128-B pixel rows.
-int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin) {
+int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld) {
   EncodeTiledFnP enc = hp_encoder();
-  if (!enc || (cin & 7) != 0) return -1;
+  if (!enc || (cin & 7) != 0 || (ld & 7) != 0) return -1;
   const HaloGeom g = halo_geom(w, 3);
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
                         static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(w) * cin * 2,
-                           static_cast<cuuint64_t>(h) * w * cin * 2};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(w) * ld * 2,
+                           static_cast<cuuint64_t>(h) * w * ld * 2};
   cuuint32_t box[4] = {64, static_cast<cuuint32_t>(g.wp), static_cast<cuuint32_t>(g.r), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,

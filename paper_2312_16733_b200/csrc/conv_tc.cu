@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int m = m0 + rsub + 8 * r4;
           if (m >= p.M) continue;
           const __nv_bfloat16* rp =
-              static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.cout + col;
+              static_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * d.ldo + col;
           in.rv[r4] = vec ? __ldg(reinterpret_cast<const uint4*>(rp)) : load_ragged_bf16x8(rp, nv);
         }
       }
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int r4 = 0; r4 < 4; ++r4) {
           const int m = m0 + rsub + 8 * r4;
           if (m >= p.M) continue;
-          const size_t off = static_cast<size_t>(m) * d.cout + col;
+          const size_t off = static_cast<size_t>(m) * d.ldo + col;
           if (!vec) {
             store_ragged8(p.y, off, nv, out_f32, o[r4][0], o[r4][1], o[r4][2], o[r4][3], o[r4][4],
                           o[r4][5], o[r4][6], o[r4][7]);
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(256) conv_finish_kernel(const __grid_constant_
     float r[8];
     if (p.res) {
       const uint4 rv = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.res) +
-                                                           m * d.cout + c));
+                                                           m * d.ldo + c));
       const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(256) conv_finish_kernel(const __grid_constant_
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] += r[q];
     if (p.out_f32) {
-      float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + m * d.cout + c);
+      float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + m * d.ldo + c);
       yp[0] = make_float4(o[0], o[1], o[2], o[3]);
       yp[1] = make_float4(o[4], o[5], o[6], o[7]);
     } else {
@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(256) conv_finish_kernel(const __grid_constant_
       pk.y = pack_bf16x2(o[2], o[3]);
       pk.z = pack_bf16x2(o[4], o[5]);
       pk.w = pack_bf16x2(o[6], o[7]);
-      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + m * d.cout + c) = pk;
+      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + m * d.ldo + c) = pk;
     }
   }
 }
@@ -887,11 +887,11 @@ int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, in
 // Residual source of a conv: [rows][cout] bf16 with {32 columns, 128 rows}
 // boxes, no swizzle (64-byte rows: the epilogue's 16-byte row-segment reads
 // of 8 lanes cover two whole rows, conflict-free).
-int make_res_map(CUtensorMap* map, const void* r, long rows, int cout) {
+int make_res_map(CUtensorMap* map, const void* r, long rows, int cout, int ld) {
   static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
-  if (!enc || (cout & 7) != 0) return -1;
+  if (!enc || (cout & 7) != 0 || (ld & 7) != 0) return -1;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cout), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cout) * 2};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
   cuuint32_t box[2] = {32, static_cast<cuuint32_t>(TC_BM)};
   cuuint32_t estr[2] = {1, 1};
   CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(r), dims, strides,
@@ -902,15 +902,15 @@ int make_res_map(CUtensorMap* map, const void* r, long rows, int cout) {
 
 // A operand: im2col map over a compact NHWC bf16 activation [n][h][w][cin]
 // for a k x k / stride / pad convolution: 128 pixels x 64 channels per load.
-int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
-                 int pad) {
+int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld, int k,
+                 int stride, int pad) {
   if (k == 1 && stride == 1 && pad == 0) {
     // pointwise conv: the activation is a plain [n*h*w][cin] matrix; a tiled
     // box {64 ch, 128 rows} is cheaper for the TMA unit than im2col mode
     static EncodeTiledFn tenc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
     if (!tenc) return -1;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(n) * h * w};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cin) * 2};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(TC_BK), static_cast<cuuint32_t>(TC_BM)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = tenc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides,
@@ -922,9 +922,9 @@ int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, 
   if (!enc) return -1;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin), static_cast<cuuint64_t>(w),
                         static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(cin) * 2,
-                           static_cast<cuuint64_t>(w) * cin * 2,
-                           static_cast<cuuint64_t>(h) * w * cin * 2};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 2,
+                           static_cast<cuuint64_t>(w) * ld * 2,
+                           static_cast<cuuint64_t>(h) * w * ld * 2};
   const int lower[2] = {-pad, -pad};
   const int upper[2] = {pad - (k - 1), pad - (k - 1)};
   cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
@@ -937,7 +937,7 @@ int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, 
   // on drivers <= 13.1 (cute/atom/copy_traits_sm90_im2col.hpp).
   int drv = 0;
   cudaDriverGetVersion(&drv);
-  const unsigned long long bytes = 2ull * n * h * w * cin;
+  const unsigned long long bytes = 2ull * n * h * w * ld;
   if (drv <= 13010 && bytes < 131072ull) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   return 0;
 }

@@ -39,6 +39,11 @@ struct alignas(64) OpDesc {
   // box {64 ch, hrows, 3 taps} at this subnet's tile width (0 = graph map)
   CUtensorMap hmap;
   int hrows;
+  // activation row strides (elements) of this op's input and output/residual
+  // buffers as THIS subnet lays them out: bf16 CNN activations pad rows to 32
+  // bytes (act_ld: 16-channel multiples) — 16-byte-aligned rows (widths
+  // = 8 mod 16) slowed every TMA read of them by up to 1.6x
+  int ldi, ldo;
 };
 
 // Active N-tile width of a tcgen05 conv: the graph-baked width bn_g (sized
@@ -233,6 +238,7 @@ struct OpDims {
   int cin, cout, k, pad;
   const float* scale;
   const float* shift;
+  int ldi, ldo;  // input / output row strides (elements)
 };
 
 __device__ __forceinline__ const OpDesc* desc_ptr(const OpDesc* const* row, const OpDesc* fixed,
@@ -242,7 +248,7 @@ __device__ __forceinline__ const OpDesc* desc_ptr(const OpDesc* const* row, cons
 
 __device__ __forceinline__ OpDims load_desc(const OpDesc* const* row, const OpDesc* fixed, int op) {
   const OpDesc* r = desc_ptr(row, fixed, op);
-  return OpDims{r->cin, r->cout, r->k, r->pad, r->scale, r->shift};
+  return OpDims{r->cin, r->cout, r->k, r->pad, r->scale, r->shift, r->ldi, r->ldo};
 }
 
 // ---------------------------------------------------------------------------

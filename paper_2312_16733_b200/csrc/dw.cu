@@ -255,14 +255,14 @@ __device__ __forceinline__ void dw_consume(const ConvParams& p, const OpDesc* dp
       for (int h = 0; h < QH; ++h) {
         const int oh = th * TH + orow + h;
         if (cok && oh < p.ho) {
-          __nv_bfloat16* yr = y + (static_cast<long>(n * p.ho + oh) * p.wo + ow0) * C + c;
+          __nv_bfloat16* yr = y + (static_cast<long>(n * p.ho + oh) * p.wo + ow0) * dp->ldo + c;
           const int nvalid = p.wo - ow0;
           if (p.act == 1)
-            dw_store_task<1, QW>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
+            dw_store_task<1, QW>(acc[h], sc, sh, yr, dp->ldo, nvalid, pool, ps);
           else if (p.act == 2)
-            dw_store_task<2, QW>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
+            dw_store_task<2, QW>(acc[h], sc, sh, yr, dp->ldo, nvalid, pool, ps);
           else
-            dw_store_task<0, QW>(acc[h], sc, sh, yr, C, nvalid, pool, ps);
+            dw_store_task<0, QW>(acc[h], sc, sh, yr, dp->ldo, nvalid, pool, ps);
         }
       }
     }
@@ -434,15 +434,15 @@ bool dw_narrow(int c_max, int stride, int wo) {
   return !off && c_max <= DW_CC_NARROW && stride == 1 && wo > 7;
 }
 
-int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int k,
+int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int ld, int k,
                     int stride, int wo, int c_max) {
   EncodeTiledFnD enc = dw_encoder();
-  if (!enc || (c & 7) != 0 || !dw_supported(7, k, stride)) return -1;
+  if (!enc || (c & 7) != 0 || (ld & 7) != 0 || !dw_supported(7, k, stride)) return -1;
   const DwShape g = dw_shape(stride, wo);
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
                         static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(w) * c * 2,
-                           static_cast<cuuint64_t>(h) * w * c * 2};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(w) * ld * 2,
+                           static_cast<cuuint64_t>(h) * w * ld * 2};
   const cuuint32_t cc = dw_narrow(c_max, stride, wo) ? DW_CC_NARROW : DW_CC;
   cuuint32_t box[4] = {cc, static_cast<cuuint32_t>((g.tw - 1) * stride + k),
                        static_cast<cuuint32_t>((g.th - 1) * stride + k), 1};

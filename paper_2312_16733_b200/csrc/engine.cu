@@ -31,21 +31,21 @@
 
 namespace ssn {
 int make_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int bn);
-int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k, int stride,
-                 int pad);
+int make_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld, int k,
+                 int stride, int pad);
 int choose_bn(int cout_max, long M, int nk_max);
 bool conv_tc_use_pairs(const ConvParams& p);
 int conv_tc_splits(const ConvParams& p);
-int make_res_map(CUtensorMap* map, const void* r, long rows, int cout);
+int make_res_map(CUtensorMap* map, const void* r, long rows, int cout, int ld);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t init_conv_halo();
 bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max);
-int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int k);
+int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld, int k);
 cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps, cudaStream_t s);
 cudaError_t init_conv_hp();
 bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max, bool graph);
-int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin);
+int make_hp_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld);
 int hp_choose_bn(int cout_max);
 int make_hp_weight_map(CUtensorMap* map, const void* w, int cin_store, int taps, int cout, int rows);
 cudaError_t launch_conv_hp(ConvParams p, const CUtensorMap& wmap, cudaStream_t s);
@@ -55,7 +55,7 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t s);
 cudaError_t launch_set_row(const OpDesc** slot, const OpDesc* row, cudaStream_t s);
 cudaError_t launch_dw_bf16(const ConvParams& p, cudaStream_t s);
-int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int k,
+int make_dw_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int c, int ld, int k,
                     int stride, int wo, int c_max);
 int dw_tiles_per_image(int stride, int ho, int wo);
 bool dw_supported(int k_max, int k, int stride);
@@ -264,6 +264,27 @@ static void* slot_ptr(ssn_engine* e, int slot, const int* map) {
     case S_LOGITS: return e->d_logits;
     default: return e->bufs[map[slot]];
   }
+}
+
+// Row stride (elements) of a `c`-channel activation buffer.  Every kernel of
+// the bf16 CNN path addresses activations through the descriptor row's
+// ldi / ldo and every TMA map takes the stride separately, so rows can be
+// padded.  SSN_PAD_ROWS=1 pads bf16 CNN rows to 16-channel multiples (32-B
+// rows; OFA widths are make_divisible(., 8), so 88, 360, 56, 104, 408, 136,
+// ... have 16-byte-aligned rows, which slowed conv_tc's im2col reads by up
+// to 1.6x in isolation, profiles/round2/align_probe_*).  Measured on the
+// networks it is a wash (R50 bs64 sweep 4052 -> 4050 us, bs256 max -3%;
+// OFA-MBv3 +1-4% from the extra bytes of 72/136/408-wide layers now that the
+// wide 14/28-px 3x3 convs read tiled windows), so rows stay compact by
+// default.  Pad channels are never read as data: TMA maps bound the channel
+// dimension at the active width, the vector epilogues touch c columns.
+static int act_ld(const ssn_engine* e, int c) {
+  static const bool pad = [] {
+    const char* v = getenv("SSN_PAD_ROWS");
+    return v && atoi(v) != 0;
+  }();
+  if (!pad || !e->bf16 || e->desc.family == SSN_FAMILY_BERT || c < 16) return c;
+  return (c + 15) & ~15;
 }
 
 // Enqueue one op (called under stream capture).
@@ -700,7 +721,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     if (e->bf16 && o.active && o.kind == OP_CONV && o.depthwise) {
       // depthwise input window map (box sized for this subnet's k)
       if (make_dw_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                          o.win, o.cout, o.k, o.stride, o.wout, o.cout_max) != 0)
+                          o.win, o.cout, act_ld(e, o.cout), o.k, o.stride, o.wout, o.cout_max) != 0)
         SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (depthwise) failed for op " + std::to_string(oi));
     }
     if (e->bf16 && o.active && (o.kind == OP_CONV || o.kind == OP_LINEAR) && !o.depthwise) {
@@ -709,11 +730,11 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
       // Shifted-window (halo) convs read a 5-D tiled map instead.
       if (use_halo(e, o)) {
         if (make_halo_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                              o.win, o.cin, o.k) != 0)
+                              o.win, o.cin, act_ld(e, o.cin), o.k) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (halo) failed for op " + std::to_string(oi));
       } else {
         if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                         o.win, o.cin, o.k, o.stride, o.k / 2) != 0)
+                         o.win, o.cin, act_ld(e, o.cin), o.k, o.stride, o.k / 2) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeIm2col failed for op " + std::to_string(oi));
         // WeightSlice B at this subnet's tile width (largest-batch graph tiling)
         if (!(tc_debug_flags() & 2097152)) {
@@ -735,7 +756,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
           const TensorSpec& t = e->net.tensors[o.tensor];
           const int hb = conv_bn_active(hp_choose_bn(o.cout_max), o.cout, 2);
           if (make_hp_act_map(&dsc.rmap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                              o.win, o.cin) != 0 ||
+                              o.win, o.cin, act_ld(e, o.cin)) != 0 ||
               make_hp_weight_map(&dsc.hmap, e->d_w + t.w_off, t.cin_store, o.k_max * o.k_max,
                                  t.cout, hb / 2) != 0)
             SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (hp) failed for op " + std::to_string(oi));
@@ -744,12 +765,15 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
         // residual source for conv_tc's TMA residual ring
         if (res_ptr[oi] && (o.cout & 7) == 0 &&
             make_res_map(&dsc.rmap, res_ptr[oi],
-                         static_cast<long>(e->desc.max_batch) * o.hout * o.wout, o.cout) != 0)
+                         static_cast<long>(e->desc.max_batch) * o.hout * o.wout, o.cout,
+                         act_ld(e, o.cout)) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (residual) failed for op " + std::to_string(oi));
       }
     }
     dsc.cin = o.cin;
     dsc.cout = o.cout;
+    dsc.ldi = act_ld(e, o.cin);
+    dsc.ldo = o.kind == OP_LINEAR ? o.cout : act_ld(e, o.cout);  // fp32 logits stay compact
     dsc.k = o.k;
     dsc.pad = o.k / 2;
     dsc.scale = nullptr;
@@ -892,7 +916,7 @@ int ssn_create(int device, const ssn_supernet_desc* desc, const void* host_weigh
     // activation arena for the largest batch at max widths
     size_t max_elems = 0;
     for (const OpSpec& o : e->net.ops)
-      max_elems = std::max(max_elems, static_cast<size_t>(o.hout) * o.wout * o.cout_max);
+      max_elems = std::max(max_elems, static_cast<size_t>(o.hout) * o.wout * act_ld(e.get(), o.cout_max));
     e->buf_bytes = max_elems * desc->max_batch * (e->bf16 ? 2 : 4);
     for (int i = 0; i < NBUF; ++i) CUDA_TRY(cudaMalloc(&e->bufs[i], e->buf_bytes));
     e->raw_img_bytes = raw_image_bytes(*desc);
@@ -1214,11 +1238,14 @@ int ssn_debug_op_checksums(ssn_engine* e, uint32_t id, uint32_t batch, uint64_t*
         const OpSpec& o = e->net.ops[sm.op];
         const OpSpec& a = sub.plan.ops[sm.op];
         const size_t elem = o.kind == OP_LINEAR ? 4 : (e->bf16 ? 2 : 4);
-        const size_t bytes = static_cast<size_t>(batch) * o.hout * o.wout * a.cout * elem;
-        host.resize(bytes);
-        CUDA_TRY(cudaMemcpy(host.data(), slot_ptr(e, o.out, sm.map), bytes, cudaMemcpyDeviceToHost));
-        uint64_t h = 1469598103934665603ull;  // FNV-1a over the op's output bytes
-        for (uint8_t b : host) h = (h ^ b) * 1099511628211ull;
+        const size_t ld = o.kind == OP_LINEAR ? a.cout : act_ld(e, a.cout);
+        const size_t rows = static_cast<size_t>(batch) * o.hout * o.wout;
+        host.resize(rows * ld * elem);
+        CUDA_TRY(cudaMemcpy(host.data(), slot_ptr(e, o.out, sm.map), host.size(),
+                            cudaMemcpyDeviceToHost));
+        uint64_t h = 1469598103934665603ull;  // FNV-1a over the op's output (active columns)
+        for (size_t r = 0; r < rows; ++r)
+          for (size_t b = 0; b < a.cout * elem; ++b) h = (h ^ host[r * ld * elem + b]) * 1099511628211ull;
         sums[sm.op] = h;
       }
     mark_done(e, s);
@@ -1261,6 +1288,8 @@ static OpDesc plain_desc(int cin, int cout, int k, int pad, const float* scale,
   std::memset(&d, 0, sizeof(d));
   d.cin = cin;
   d.cout = cout;
+  d.ldi = cin;  // operator API: compact caller tensors
+  d.ldo = cout;
   d.k = k;
   d.pad = pad;
   d.scale = scale;
@@ -1311,8 +1340,8 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
                     (cout_max & 7) == 0 && aligned16 && !(getenv("SSN_OP_NO_HP")) &&
                     hp_eligible(h, w, k, stride, cin_max, cout_max, false);
     OpDesc d = plain_desc(cin, cout, k, pad, scale, shift);
-    if (!hp && (halo ? make_halo_act_map(&d.amap, x, n, h, w, cin, k) != 0
-                     : make_act_map(&d.amap, x, n, h, w, cin, k, stride, pad) != 0))
+    if (!hp && (halo ? make_halo_act_map(&d.amap, x, n, h, w, cin, cin, k) != 0
+                     : make_act_map(&d.amap, x, n, h, w, cin, cin, k, stride, pad) != 0))
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncode (activation) failed");
     ConvParams p{};
     p.x = x;
@@ -1342,7 +1371,7 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
       p.bn = hp_choose_bn(cout_max);
       const int bn_a = conv_bn_active(p.bn, cout, 2);
       OpDesc d2 = d;
-      if (make_hp_act_map(&d2.rmap, x, n, h, w, cin) != 0 ||
+      if (make_hp_act_map(&d2.rmap, x, n, h, w, cin, cin) != 0 ||
           make_hp_weight_map(&d2.hmap, wgt, cin_max, k * k, cout_max, bn_a / 2) != 0)
         SSN_THROW(SSN_E_CUDA, "cuTensorMapEncode (hp) failed");
       d2.hrows = bn_a / 2;
@@ -1379,7 +1408,7 @@ int ssn_op_dw_bf16(const void* x, int n, int h, int w, int c, const void* wgt, i
     const int pad = k / 2;
     const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
     OpDesc d = plain_desc(c, c, k, pad, scale, shift);
-    if (make_dw_act_map(&d.amap, x, n, h, w, c, k, stride, wo, c_max) != 0)
+    if (make_dw_act_map(&d.amap, x, n, h, w, c, c, k, stride, wo, c_max) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (depthwise) failed");
     ConvParams p{};
     p.x = x;

@@ -308,12 +308,17 @@ __global__ void __launch_bounds__(STEM_THREADS) stem_conv_kernel(StemParams p) {
       }
     }
     __syncthreads();
-    // the output row is contiguous: wo * cout bf16 (16-byte multiple: cout % 8 == 0)
-    const int nvec = p.wo * cout / 8;
+    // the output row: wo pixels of cout bf16 at the row stride d.ldo (16-byte
+    // multiples: cout % 8 == 0)
+    const int npx = cout / 8, ld8 = d.ldo / 8;
+    const int nvec = p.wo * npx;
     uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) +
-                                          (static_cast<long>(img) * p.ho + oh) * p.wo * cout);
+                                          (static_cast<long>(img) * p.ho + oh) * p.wo * d.ldo);
     const uint4* src = reinterpret_cast<const uint4*>(s_out);
-    for (int i = tid; i < nvec; i += STEM_THREADS) dst[i] = src[i];
+    for (int i = tid; i < nvec; i += STEM_THREADS) {
+      const int px = i / npx;
+      dst[px * ld8 + (i - px * npx)] = src[i];
+    }
     __syncthreads();  // s_out is rewritten by the next row
   }
 }
@@ -354,11 +359,11 @@ __global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
   const int g = threadIdx.x & 7, lane = threadIdx.x >> 3;
   const int c = c0 + g * 8;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * hw * C;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * hw * d.ldi;
   if (c < C) {
     for (int q = lane; q < hw; q += 32) {
       float f[8];
-      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * C + c)), f);
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * d.ldi + c)), f);
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] += f[t];
     }
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
   if (threadIdx.x < 64 && c0 + threadIdx.x < C) {
     float sum = 0.f;
     for (int l = 0; l < 32; ++l) sum += red[l][threadIdx.x];
-    static_cast<__nv_bfloat16*>(p.y)[static_cast<long>(n) * C + c0 + threadIdx.x] =
+    static_cast<__nv_bfloat16*>(p.y)[static_cast<long>(n) * d.ldo + c0 + threadIdx.x] =
         __float2bfloat16_rn(sum / static_cast<float>(hw));
   }
 }
@@ -401,7 +406,7 @@ __global__ void __launch_bounds__(256) pool_k_bf16_kernel(PoolParams p) {
       ok[r * K + s2] = ih >= 0 && ih < p.h && iw >= 0 && iw < p.w;
       v[r * K + s2] = ok[r * K + s2]
                           ? __ldg(reinterpret_cast<const uint4*>(
-                                x + (static_cast<size_t>(img * p.h + ih) * p.w + iw) * C))
+                                x + (static_cast<size_t>(img * p.h + ih) * p.w + iw) * d.ldi))
                           : make_uint4(0, 0, 0, 0);
     }
   float acc[8];
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(256) pool_k_bf16_kernel(PoolParams p) {
     for (int t = 0; t < 8; ++t) acc[t] *= inv;
   }
   *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) +
-                            (static_cast<size_t>(row) * p.wo + ow) * C + g * 8) = f32_to_bf16x8(acc);
+                            (static_cast<size_t>(row) * p.wo + ow) * d.ldo + g * 8) = f32_to_bf16x8(acc);
 }
 
 __global__ void pool_bf16_kernel(PoolParams p) {
@@ -442,16 +447,16 @@ __global__ void pool_bf16_kernel(PoolParams p) {
       const long img = i / G;
       const int g = static_cast<int>(i - img * G);
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const __nv_bfloat16* src = x + img * hw * C + g * 8;
+      const __nv_bfloat16* src = x + img * hw * d.ldi + g * 8;
       for (int q = 0; q < hw; ++q) {
         float f[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(src + static_cast<long>(q) * C), f);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(src + static_cast<long>(q) * d.ldi), f);
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[t] += f[t];
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] *= inv;
-      *reinterpret_cast<uint4*>(y + img * C + g * 8) = f32_to_bf16x8(acc);
+      *reinterpret_cast<uint4*>(y + img * d.ldo + g * 8) = f32_to_bf16x8(acc);
     }
     return;
   }
@@ -475,7 +480,7 @@ __global__ void pool_bf16_kernel(PoolParams p) {
         if (iw < 0 || iw >= p.w) continue;
         float f[8];
         bf16x8_to_f32(
-            *reinterpret_cast<const uint4*>(x + ((img * p.h + ih) * p.w + iw) * C + g * 8), f);
+            *reinterpret_cast<const uint4*>(x + ((img * p.h + ih) * p.w + iw) * d.ldi + g * 8), f);
         ++cnt;
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[t] = p.kind == 2 ? fmaxf(acc[t], f[t]) : acc[t] + f[t];
@@ -486,7 +491,7 @@ __global__ void pool_bf16_kernel(PoolParams p) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] *= inv;
     }
-    *reinterpret_cast<uint4*>(y + opix * C + g * 8) = f32_to_bf16x8(acc);
+    *reinterpret_cast<uint4*>(y + opix * d.ldo + g * 8) = f32_to_bf16x8(acc);
   }
 }
 
@@ -598,11 +603,11 @@ __global__ void se_pool_kernel(SEParams p) {
   const int g = threadIdx.x & 7, lane = threadIdx.x >> 3;
   const int c = c0 + g * 8;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * p.hw * C;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * p.hw * d.ldi;
   if (c < C) {
     for (int q = lane; q < p.hw; q += 32) {
       float f[8];
-      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * C + c)), f);
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * d.ldi + c)), f);
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] += f[t];
     }
@@ -734,7 +739,7 @@ __global__ void se_scale_kernel(SEParams p) {
     const long pix = i / G;
     const int g = static_cast<int>(i - pix * G);
     const int n = static_cast<int>(pix / p.hw);
-    uint4* ptr = reinterpret_cast<uint4*>(x + pix * C + g * 8);
+    uint4* ptr = reinterpret_cast<uint4*>(x + pix * d.ldi + g * 8);
     float f[8];
     bf16x8_to_f32(*ptr, f);
     const float* gt = p.gate + static_cast<long>(n) * p.c_max + g * 8;
