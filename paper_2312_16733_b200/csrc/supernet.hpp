@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/ssn.h"
@@ -139,6 +140,15 @@ inline int rnd(double v) { return ssn_round_half_even(v); }
 // ---------------------------------------------------------------------------
 // builder helpers
 
+// A/B switch for the padded weight rows (SSN_PACK_WEIGHTS=1: compact rows)
+inline bool pad16_weights() {
+  static const bool off = [] {
+    const char* v = std::getenv("SSN_PACK_WEIGHTS");
+    return v && std::atoi(v) != 0;
+  }();
+  return !off;
+}
+
 class Builder {
  public:
   explicit Builder(Net& n) : net(n) {}
@@ -150,6 +160,13 @@ class Builder {
     t.k = k;
     t.depthwise = dw;
     t.linear = linear;
+    // pad16: bf16 CNN supernets store every conv / linear row at a 16-channel
+    // multiple (32-B rows, zero pad): TMA reads of 16-B-aligned rows (stored
+    // widths 88, 360, 56, 104, 136 ... = 8 mod 16) ran at half rate
+    // (tools/ubench/tma_rate.cu: 720-B pitch 97 vs 736-B 146 B/cycle/SM).
+    // The pad channels meet zero-filled activations (maps bound the channel
+    // dimension at the active width), so they never contribute.
+    if (!cin_store && pad16 && !dw) cin_store = (cin + 15) & ~15;
     t.cin_store = dw ? 1 : (cin_store ? cin_store : cin);
     t.fan_in = static_cast<uint32_t>(t.cin * k * k);
     net.tensors.push_back(t);
@@ -187,6 +204,7 @@ class Builder {
 
   Net& net;
   int cur_segment = -1;
+  bool pad16 = false;
 };
 
 inline void finalize_layout(Net& net) {
@@ -423,6 +441,7 @@ inline Net build_ofa_resnet50(const ssn_supernet_desc& d, const SubnetCfg* cfg) 
   const bool bf16 = d.dtype == SSN_DTYPE_BF16;
   net.elem_bytes = bf16 ? 2 : 4;
   Builder b(net);
+  b.pad16 = bf16 && pad16_weights();
   const int H = static_cast<int>(d.image_size);
   const int stem_mid_a = md8(md8(64 * s.width[0]) / 2);
   const int stem_out_a = md8(64 * s.width[1]);
@@ -650,6 +669,7 @@ inline Net build_ofa_mbv3(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
   if (d.dtype != SSN_DTYPE_BF16) throw std::invalid_argument("ofa_mbv3 runs in bf16");
   net.elem_bytes = 2;
   Builder b(net);
+  b.pad16 = pad16_weights();
   const int H = static_cast<int>(d.image_size);
   const int H2 = (H + 2 - 3) / 2 + 1;
 
@@ -722,8 +742,9 @@ inline Net build_ofa_mbv3(const ssn_supernet_desc& d, const SubnetCfg* cfg) {
       int tr = -1, te = -1;
       const int se_max = md8(mid_max / 4);
       if (SE[st]) {
-        tr = b.tensor(se_max, mid_max, 1, false, true);  // reduce (+bias)
-        te = b.tensor(mid_max, se_max, 1, false, true);  // expand (+bias)
+        // SE FCs keep compact rows (se_fc_kernel's row strides: c_max / se_max)
+        tr = b.tensor(se_max, mid_max, 1, false, true, mid_max);  // reduce (+bias)
+        te = b.tensor(mid_max, se_max, 1, false, true, se_max);   // expand (+bias)
       }
       const int tp = b.tensor(cout, mid_max, 1, false, false);
       const int np = b.norm(cout, res);
