@@ -54,6 +54,10 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (64, 14, 14, 1024, 1024, 368, 368, 1, 1, 0),     # 39: = case32 at a 32-B aligned width
     (64, 14, 14, 1024, 1024, 384, 384, 1, 1, 0),     # 40: = case32 at a 128-B aligned width
     (64, 14, 14, 384, 384, 1024, 1024, 1, 1, 1),     # 41: = case5 with an aligned input
+    (64, 14, 14, 360, 368, 360, 360, 3, 1, 0),       # 42: case2 with 32-B weight rows (engine store)
+    (64, 14, 14, 1024, 1024, 360, 360, 1, 1, 0),     # 43: = case32 (aligned weights already)
+    (64, 14, 14, 360, 368, 1024, 1024, 1, 1, 1),     # 44: case5 with 32-B weight rows
+    (256, 14, 14, 360, 368, 360, 360, 3, 1, 0),      # 45: case26 with 32-B weight rows
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):

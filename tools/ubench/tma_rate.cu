@@ -58,12 +58,15 @@ void run(CUtensorMap map, int rows_total, long long* d) {
 }
 
 int main(int argc, char** argv) {
+  // argv[2] = row pitch in bytes (default 128: contiguous rows; e.g. 6480 =
+  // the KRSC pitch of a 3x3 x 360-channel weight tensor)
   // default 16384 x 64 bf16 = 2 MB (L2 resident, shared by all SMs); argv[1]
   // = rows, e.g. 1048576 (128 MB: each SM streams its own, mostly distinct data)
   const int rows = argc > 1 ? atoi(argv[1]) : 16384;
+  const long pitch = argc > 2 ? atol(argv[2]) : 128;
   void* src;
-  cudaMalloc(&src, rows * 128);
-  cudaMemset(src, 0, rows * 128);
+  cudaMalloc(&src, rows * pitch);
+  cudaMemset(src, 0, rows * pitch);
   long long* d;
   cudaMalloc(&d, 148 * 8);
   using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -76,7 +79,7 @@ int main(int argc, char** argv) {
   auto mk = [&](int box_rows) {
     CUtensorMap m;
     cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {128};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch)};
     cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
     enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box, estr,
