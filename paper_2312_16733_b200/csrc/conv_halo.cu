@@ -40,6 +40,7 @@ constexpr int HL_MMA_WARP = 1 + HL_EPI_WARPS;
 constexpr int HL_THREADS = (HL_MMA_WARP + 1) * 32;
 constexpr int HL_SMEM_MAX = 232448;  // 227 KB opt-in
 constexpr int HL_CB = 32;            // channels per A stage (two K=16 steps)
+constexpr int HL_MAX_STAGES = 8;
 
 __global__ void __launch_bounds__(HL_THREADS, 1)
     conv_halo_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
@@ -70,26 +71,37 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   // starts (r*Wp + s) rows into the window: the tensor core applies the
   // swizzle on absolute smem address bits, so any 64-B row offset is a legal
   // start (verified exact on B200: tools/ubench/sw128_shift.cu -DSW64).
-  const int ncb_max = p.hb_chunks;                                      // 32-ch blocks (max shape)
-  const uint32_t b_blk = static_cast<uint32_t>(p.hb_rows) * 64;        // one (tap, cb) block
-  const uint32_t b_bytes = b_blk * static_cast<uint32_t>(ka * ka * ncb_max);
+  // Resident B at the ACTIVE width when the subnet row carries its own halo
+  // weight map (wmap slot, box rows = wrows = the 16-rounded active cout):
+  // only the active 32-channel blocks and rows are loaded, and the shared
+  // memory a narrow subnet leaves free deepens the window ring (e.g. OFA-R50
+  // mid at 56 px: 74 of the max shape's 166 KB, 3 -> 8 stages).  A row
+  // without one (operator API) uses the graph's max-width map.
+  const bool own_b = dp->wrows == bn;
+  const CUtensorMap* wm = own_b ? &dp->wmap : &wmap;
+  const int ncb_b = own_b ? ncb : p.hb_chunks;                          // resident 32-ch blocks
+  const uint32_t b_blk = static_cast<uint32_t>(own_b ? bn : p.hb_rows) * 64;  // one (tap, cb) block
+  const uint32_t b_bytes = b_blk * static_cast<uint32_t>(ka * ka * ncb_b);
   const uint32_t a_box = static_cast<uint32_t>(R * wp) * 64;           // TMA box bytes
   const uint32_t a_stage = (a_box + 1023) & ~1023u;                    // swizzle-atom aligned
-  const int ST = p.h_stages;
-  uint8_t* sB = smem;
-  uint8_t* sA = smem + ((b_bytes + 1023) & ~1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + ST * a_stage);
-  uint64_t* full = bars;
-  uint64_t* empty = full + ST;
-  uint64_t* tfull = empty + ST;    // [4]
-  uint64_t* tempty = tfull + 4;    // [4]
+  // [barriers + SubnetNorm vectors: 2 KB][resident B][A ring]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = bars;                         // [HL_MAX_STAGES]
+  uint64_t* empty = full + HL_MAX_STAGES;
+  uint64_t* tfull = empty + HL_MAX_STAGES;       // [4]
+  uint64_t* tempty = tfull + 4;                  // [4]
   uint64_t* bfull = tempty + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 2);
   // SubnetNorm scale / shift of this op (cout <= 128), staged once: the
   // row-per-lane epilogue reads all columns per lane, and per-column global
   // loads issued right before their FMAs serialised an L1/L2 round trip per
   // 8 columns (ncu: the epilogue's FFMAs were the top stall site)
-  float* sn = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));  // [2][128]
+  float* sn = reinterpret_cast<float*>(smem + 1024);  // [2][128]
+  uint8_t* sB = smem + 2048;
+  uint8_t* sA = sB + ((b_bytes + 1023) & ~1023u);
+  int ST = static_cast<int>((static_cast<uint32_t>(p.h_smem) - 2048u - ((b_bytes + 1023) & ~1023u)) /
+                            a_stage);
+  ST = ST > HL_MAX_STAGES ? HL_MAX_STAGES : ST;
 
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through shfl: the compiler then knows it is warp-uniform, so
@@ -106,7 +118,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     }
     mbar_init(bfull, 1);
     fence_mbar_init();
-    tma_prefetch(&wmap);
+    tma_prefetch(wm);
     tma_prefetch(&dp->amap);
   }
   if (warp == HL_MMA_WARP) tmem_alloc(tmem_slot, 512);
@@ -141,8 +153,8 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
       mbar_arrive_expect_tx(bfull, b_bytes);
       for (int r = 0; r < ka; ++r)
         for (int s = 0; s < ka; ++s)
-          for (int cb = 0; cb < ncb_max; ++cb)
-            tma_load_3d(sB + ((r * ka + s) * ncb_max + cb) * b_blk, &wmap, bfull, cb * HL_CB,
+          for (int cb = 0; cb < ncb_b; ++cb)
+            tma_load_3d(sB + ((r * ka + s) * ncb_b + cb) * b_blk, wm, bfull, cb * HL_CB,
                         (r + koff) * p.k_max + (s + koff), 0);
     }
     const CUtensorMap* amap = &dp->amap;
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     const uint64_t a_base = umma_desc_sw64(smem_u32(sA));
     const uint64_t b_base = umma_desc_sw64(smem_u32(sB));
     const uint32_t a_st16 = a_stage >> 4;
-    const uint32_t b_tap16 = (ncb_max * b_blk) >> 4, b_cb16 = b_blk >> 4;
+    const uint32_t b_tap16 = (ncb_b * b_blk) >> 4, b_cb16 = b_blk >> 4;
     constexpr uint32_t ks16 = 2;  // K=16 step inside a 64-B row: +32 B
     HL_WAIT(w_wait, bfull, 0);
     tc_fence_after();
@@ -370,9 +382,9 @@ static void halo_sizes(int w, int k_max, int cin_max, int cout_max, long* b_byte
 static int halo_stages(int w, int k_max, int cin_max, int cout_max) {
   long bb, as;
   halo_sizes(w, k_max, cin_max, cout_max, &bb, &as);
-  const long avail = HL_SMEM_MAX - 1024 - ((bb + 1023) & ~1023L) - 256 - 2 * 128 * 4;
+  const long avail = HL_SMEM_MAX - 1024 - 2048 - ((bb + 1023) & ~1023L);
   const long st = avail / as;
-  return static_cast<int>(st > 6 ? 6 : st);
+  return static_cast<int>(st > HL_MAX_STAGES ? HL_MAX_STAGES : st);
 }
 
 // The shifted-window kernel serves stride-1 odd k x k convs whose max-shape
@@ -410,8 +422,8 @@ int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int 
 
 // B operand: max-shape KRSC [cout][taps][cin_store], box {32 ch, 1 tap, rows}
 // with 64-byte swizzle: one (tap, 32-channel block) of the weight slice.
-static int make_halo_weight_map(CUtensorMap* map, const void* wgt, int cin_store, int taps,
-                                int cout, int rows, int /*chunks*/) {
+int make_halo_weight_map(CUtensorMap* map, const void* wgt, int cin_store, int taps, int cout,
+                         int rows, int /*chunks*/) {
   EncodeTiledFnH enc = tiled_encoder();
   if (!enc) return -1;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin_store), static_cast<cuuint64_t>(taps),
@@ -460,8 +472,12 @@ cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int t
     return cudaErrorInvalidValue;
   long bb, as;
   halo_sizes(p.w_, p.k_max, p.cin_max, p.cout_max, &bb, &as);
-  const long smem = 1024 + ((bb + 1023) & ~1023L) + p.h_stages * as + (2 * p.h_stages + 9) * 8 + 16 +
-                    2 * 128 * 4 + 32;
+  // the whole opt-in shared memory: a narrow subnet turns the part of the
+  // max-shape B region it does not use into extra ring stages
+  (void)bb;
+  (void)as;
+  const long smem = HL_SMEM_MAX;
+  p.h_smem = static_cast<int>(smem - 1024);
   const HaloGeom g = halo_geom(p.w_, p.k_max);
   const long tiles = static_cast<long>(p.n) * ((p.h + g.rt - 1) / g.rt);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());

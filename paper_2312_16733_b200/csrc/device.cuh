@@ -168,6 +168,7 @@ struct ConvParams {
   int cg2;            // weight map boxes hold bn/2 rows: 2-CTA pair tiles (conv_tc CG = 2)
   // halo kernel (conv_halo.cu): resident weight box rows / K chunks, A ring depth
   int hb_rows, hb_chunks, h_stages;
+  int h_smem;         // conv_halo: dynamic shared memory past the 1 KB alignment slack
   // split-K (conv_tc): `splits` K ranges per tile write raw fp32 sums to
   // `ws` ([splits][M][cout_a]); conv_finish_kernel adds them + the epilogue
   int splits;

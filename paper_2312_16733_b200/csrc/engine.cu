@@ -42,6 +42,8 @@ cudaError_t init_conv_tc();
 cudaError_t init_conv_halo();
 bool halo_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max);
 int make_halo_act_map(CUtensorMap* map, const void* x, int n, int h, int w, int cin, int ld, int k);
+int make_halo_weight_map(CUtensorMap* map, const void* wgt, int cin_store, int taps, int cout,
+                         int rows, int chunks);
 cudaError_t launch_conv_halo(ConvParams p, const void* wgt, int cin_store, int taps, cudaStream_t s);
 cudaError_t init_conv_hp();
 bool hp_eligible(int h, int w, int k_max, int stride, int cin_max, int cout_max, bool graph);
@@ -729,9 +731,16 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
       // activation (cin_a channels) in the buffer its graph variant reads.
       // Shifted-window (halo) convs read a 5-D tiled map instead.
       if (use_halo(e, o)) {
+        // resident B at this subnet's width (rows = 16-rounded cout_a, only
+        // the active 32-channel blocks are loaded): wmap slot, wrows = rows
+        const TensorSpec& t = e->net.tensors[o.tensor];
+        const int hrows = (o.cout + 15) & ~15;
         if (make_halo_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
-                              o.win, o.cin, act_ld(e, o.cin), o.k) != 0)
+                              o.win, o.cin, act_ld(e, o.cin), o.k) != 0 ||
+            make_halo_weight_map(&dsc.wmap, e->d_w + t.w_off, t.cin_store, o.k_max * o.k_max,
+                                 t.cout, hrows, 0) != 0)
           SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (halo) failed for op " + std::to_string(oi));
+        dsc.wrows = hrows;
       } else {
         if (make_act_map(&dsc.amap, in_ptr[oi], static_cast<int>(e->desc.max_batch), o.hin,
                          o.win, o.cin, act_ld(e, o.cin), o.k, o.stride, o.k / 2) != 0)
