@@ -758,8 +758,8 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
           dsc.wrows = bn_a / cg;
         }
         // shifted-window pair kernel (large-batch graphs of residual-free
-        // 14-px 3x3 convs): its 4-D window map rides in the unused rmap slot
-        // (B comes from the graph's max-width map), so the same subnet row
+        // 28- and 14-px 3x3 convs): its 4-D window map rides in the unused
+        // rmap slot and its filter-row B map in hmap, so the same subnet row
         // also serves the small-batch graphs' conv_tc
         if (use_hp(e, o, e->desc.max_batch)) {
           const TensorSpec& t = e->net.tensors[o.tensor];
