@@ -166,13 +166,19 @@ __global__ void input_im2col_kernel(InputParams p) {
 // registers, the row is staged in shared memory and leaves as contiguous
 // 16-byte stores.  Replaces input_im2col3 + a K = 32 GEMM that wrote and
 // re-read a 32-channel im2col tensor (2 x 51 MB at bs64 x 224 px).
-constexpr int STEM_THREADS = 128;
+#ifndef SSN_STEM_THREADS
+#define SSN_STEM_THREADS 128
+#endif
+#ifndef SSN_STEM_RPC
+#define SSN_STEM_RPC 8  // 8 output rows per CTA: MBv3 bs256 stem 119 -> 109 us (2 / 4 rows slower; 256 threads slower)
+#endif
+constexpr int STEM_THREADS = SSN_STEM_THREADS;
 constexpr int STEM_MAXW = 256;                       // input width bound (engine checks)
 // staged input row (bf16): [5 unused][left zero pixel: 3][w pixels x 3][right zero pixel: 3],
 // pixel data 16-byte aligned at element 8
 constexpr int STEM_SROW = 8 + (STEM_MAXW + 1) * 3 + 5;
 constexpr int STEM_COUT = 32;                        // max stem width (4 n8 tiles)
-constexpr int STEM_RPC = 4;                          // output rows per CTA
+constexpr int STEM_RPC = SSN_STEM_RPC;               // output rows per CTA
 constexpr int STEM_IN_ROWS = 2 * STEM_RPC + 1;       // input rows they read
 
 __global__ void __launch_bounds__(STEM_THREADS) stem_conv_kernel(StemParams p) {
