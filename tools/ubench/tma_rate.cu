@@ -7,7 +7,25 @@
 #include "device.cuh"
 using namespace ssn;
 
-template <int STAGES, int BOX_ROWS, int P>
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+#ifdef SPIN
+#define WAIT mbar_spin
+#else
+#define WAIT mbar_wait
+#endif
+template <int STAGES, int BOX_ROWS, int P, int SPLIT = 1>
 __global__ void __launch_bounds__(256, 1) k(const __grid_constant__ CUtensorMap map, int iters, int rows_total,
                                           long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -24,37 +42,51 @@ __global__ void __launch_bounds__(256, 1) k(const __grid_constant__ CUtensorMap 
   }
   __syncthreads();
   long long t0 = clock64();
-  if (warp < P && lane == 0) {  // P producer warps, each owning stages s = warp (mod P)
-    for (int g = warp; g < iters; g += P) {
+#ifdef LANES
+  const bool prod = warp == 0 && lane < P;  // P producer LANES of warp 0
+  const int pid = lane;
+#else
+  const bool prod = warp < P && lane == 0;  // P producer warps
+  const int pid = warp;
+#endif
+  if (prod) {  // producer pid owns stages s = pid (mod P)
+    for (int g = pid; g < iters; g += P) {
       const int s = g % STAGES;
-      mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+      WAIT(&empty[s], ((g / STAGES) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], BYTES);
       const int row = static_cast<int>((static_cast<long>(blockIdx.x) * (rows_total / 148) + static_cast<long>(g) * BOX_ROWS) % (rows_total - BOX_ROWS));
-      tma_load_2d(buf + s * BYTES, &map, &full[s], 0, row);
+#pragma unroll
+      for (int q = 0; q < SPLIT; ++q)  // SPLIT boxes of BOX_ROWS / SPLIT rows per stage
+        tma_load_2d(buf + s * BYTES + q * (BYTES / SPLIT), &map, &full[s], 0, row + q * (BOX_ROWS / SPLIT));
     }
-  } else if (warp == P && lane == 0) {
+  }
+#ifdef LANES
+  else if (warp == 1 && lane == 0) {
+#else
+  else if (warp == P && lane == 0) {
+#endif
     for (int g = 0; g < iters; ++g) {
       const int s = g % STAGES;
-      mbar_wait(&full[s], (g / STAGES) & 1);
+      WAIT(&full[s], (g / STAGES) & 1);
       mbar_arrive(&empty[s]);
     }
     out[blockIdx.x] = clock64() - t0;
   }
 }
 
-template <int STAGES, int BOX_ROWS, int P>
+template <int STAGES, int BOX_ROWS, int P, int SPLIT = 1>
 void run(CUtensorMap map, int rows_total, long long* d) {
   const int iters = 2000;
   const int smem = STAGES * BOX_ROWS * 128 + 1024;
-  cudaFuncSetAttribute(k<STAGES, BOX_ROWS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int rep = 0; rep < 2; ++rep) k<STAGES, BOX_ROWS, P><<<148, 256, smem>>>(map, iters, rows_total, d);
+  cudaFuncSetAttribute(k<STAGES, BOX_ROWS, P, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int rep = 0; rep < 2; ++rep) k<STAGES, BOX_ROWS, P, SPLIT><<<148, 256, smem>>>(map, iters, rows_total, d);
   cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double mx = 0;
   for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-  printf("producers=%d stages=%2d box=%3d rows (%5d B): %6.1f B/cycle/SM (slowest SM)\n", P, STAGES,
-         BOX_ROWS, BOX_ROWS * 128, double(iters) * BOX_ROWS * 128 / mx);
+  printf("producers=%d stages=%2d stage=%3d rows (%5d B) in %d box(es): %6.1f B/cycle/SM (slowest SM)\n", P,
+         STAGES, BOX_ROWS, BOX_ROWS * 128, SPLIT, double(iters) * BOX_ROWS * 128 / mx);
 }
 
 int main(int argc, char** argv) {
@@ -98,5 +130,10 @@ int main(int argc, char** argv) {
   run<4, 256, 2>(mk(256), rows, d);
   run<3, 256, 2>(mk(256), rows, d);
   run<4, 256, 1>(mk(256), rows, d);
+  // per-wait vs per-issue cost: the same stage bytes in 1, 2 or 4 boxes
+  run<8, 256, 1, 2>(mk(128), rows, d);
+  run<8, 256, 1, 4>(mk(64), rows, d);
+  run<8, 128, 1, 2>(mk(64), rows, d);
+  run<8, 256, 2, 2>(mk(128), rows, d);
   return 0;
 }
