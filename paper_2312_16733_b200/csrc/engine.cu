@@ -304,9 +304,15 @@ static bool use_halo(const ssn_engine* e, const OpSpec& o) {
 // Wider stride-1 3x3 convs without a residual (OFA-R50 3x3 at 28 / 14 px)
 // run the 2-CTA shifted-window kernel (conv_hp.cu); same max-shape rule.
 static bool use_hp(const ssn_engine* e, const OpSpec& o, uint32_t batch) {
-  // small batches: conv_tc's split-K spreads the few tiles better (bs1 max
-  // 630 vs 665 us); from 32 images on the pair kernel wins (bs256 max -1.6%)
-  if (batch < 32) return false;
+  // bs 1-2: conv_tc's split-K spreads the few tiles better for the wide
+  // (max-subnet) layers (bs1 max 635 vs 651 us); from 4 images on the pair
+  // kernel wins for every subnet (bs4 mid 514 -> 491, bs16 mid 657 -> 628,
+  // bs16 max 936 -> 911 us; SSN_HP_MIN_BATCH overrides)
+  static const uint32_t min_batch = [] {  // A/B knob (SSN_HP_MIN_BATCH)
+    const char* v = getenv("SSN_HP_MIN_BATCH");
+    return v ? static_cast<uint32_t>(atoi(v)) : 4u;
+  }();
+  if (batch < min_batch) return false;
   if (!e->bf16 || o.kind != OP_CONV || o.depthwise || o.act > 1 || o.res != S_NONE ||
       (o.cout_max & 7) != 0 || use_halo(e, o))
     return false;
