@@ -21,6 +21,8 @@ switch, so the SubNetAct actuation path is inside the timed region.
   families  configs 3 (OFA-MBv3, bs 16-512) and 5 (BERT seq 128) batch sweeps
   cpu_baseline / cpu_baseline_families  the CPU oracle (fp32 port, all host
             threads) on bounded samples (rank 0, N = 1 only)
+  cpu_baseline_torch  the config-2 sweep on a tuned CPU path (torch/oneDNN,
+            extracted subnets, bs8, all host threads), informational
   parity    image 0 of each timed subnet against the oracle (checker, untimed)
 
 Multi-GPU: one process per GPU; ``--gpus N`` under plain python re-executes
@@ -187,6 +189,21 @@ def cpu_families(seconds=3.0):
     return out
 
 
+def cpu_torch_sweep(args):
+    """Informational: the same sweep on a TUNED CPU path (torch / oneDNN,
+    extracted subnets, folded SubnetNorm, channels_last, all host threads;
+    tests/golden/cpu_torch.py).  The oracle stays the cpu_baseline / reference
+    arm; this row says what a real CPU deployment of the workload would do."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        import cpu_torch
+        r = cpu_torch.r50_sweep(args.image, batch=8, seconds=args.cpu_seconds)
+        r["model"] = cpu_model()
+        return r
+    except Exception as e:  # informational only; never fails the bench line
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -345,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
     roof = driver_roofline(eng, desc, cfgs, B, peaks, ssn, ms / args.steps)
     parity = None if args.no_parity else parity_check(eng, cfgs, xs[0], B, stream)
     families = None if args.no_families else family_rows(ssn, peaks, local_rank, args.quick)
-    cpu = cpu_fam = None
+    cpu = cpu_fam = cpu_torch = None
     if world == 1 and not args.no_cpu:
         n, el, cores = cpu_sample(args.image, 1, min_seconds=args.cpu_seconds, max_rounds=8)
         cpu = {"value": n / el, "unit": "images/s", "cores": cores, "kind": "port",
@@ -353,6 +370,7 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"{n} images over {{{','.join(SUBNETS)}}} (1 per subnet per round) at "
                          f"{args.image}x{args.image}, fp32, {el:.1f} s"}
         cpu_fam = cpu_families(seconds=3.0)
+        cpu_torch = cpu_torch_sweep(args)
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -375,6 +393,7 @@ def run_ours(args, rank, world, local_rank):
         "families": families,
         "cpu_baseline": cpu,
         "cpu_baseline_families": cpu_fam,
+        "cpu_baseline_torch": cpu_torch,
         "parity": parity,
         "engine": {k: v for k, v in eng.stats().items()
                    if k in ("weight_bytes", "norm_table_bytes", "arena_bytes", "graphs_built")},
