@@ -168,44 +168,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
-  // WeightSlice tile width of the actuated subnet (conv_bn_active); its own
-  // weight map (box = bn / CG rows) when the subnet row carries one that
-  // matches, else the graph's max-width map (extra rows land unused)
-  const int bn = (p.dbg & 4194304) ? p.bn : conv_bn_active(p.bn, d.cout, CG);  // A/B switch
-  const bool own_wmap = dp->wrows == bn / CG;
-  const CUtensorMap* wm = own_wmap ? &dp->wmap : &wmap;
-  const int brows = own_wmap ? bn / CG : p.bn / CG;  // rows each B box lands
-  const int mt = (p.M + TC_BM * CG - 1) / (TC_BM * CG);  // CG = 2: 256-row pair tiles
-  const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
-  const int tiles = mt * nt;
-  const int S = p.splits > 1 ? p.splits : 1;  // split-K: work unit u = (tile u / S, K range u % S)
-  const int units = tiles * S;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
-  const int unit0 = static_cast<int>(blockIdx.x) / CG;     // this CTA's (pair's) first tile
-  const int ustep = static_cast<int>(gridDim.x) / CG;
-  if (unit0 >= units) return;  // both CTAs of a pair agree
-  // Epilogue work split: wide tiles (>= TC_EPI_GROUPS 32-column chunks) are
-  // striped chunk-wise across all groups; narrow ones go whole to one group
-  // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
-  // (a narrow ACTIVE width on a wide instance stripes too: the alternate mode
-  // needs NACC % 3 == 0, which only the 64-wide instances guarantee)
-  const bool stripe = (bn + 31) / 32 >= TC_EPI_GROUPS || C::NACC % TC_EPI_GROUPS != 0;
-  // alternate mode hands tile i to group i % 3 and accumulator i % NACC: the
-  // pair must be a function of the accumulator alone
-  static_assert(BN_MAX > 64 || C::NACC % TC_EPI_GROUPS == 0, "accumulator/group mapping");
+  const int d_wrows = dp->wrows;
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through shfl: the compiler then knows it is warp-uniform, so
   // role branches stay uniform and MMA/TMA operands live in uniform registers
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
 
-  const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
-  const int cblocks = (d.cin + TC_BK - 1) / TC_BK;
-  const int nk = ka * ka * cblocks;
-  // resident B: K blocks packed at the ACTUAL tile width (bn rows of 128 B,
-  // a multiple of the 1 KB swizzle atom), which is what resident_b() sizes
-  // against TC_RB_BYTES — a BN_MAX stride overran the region for bn < BN_MAX
-  const uint32_t rb_stride = static_cast<uint32_t>(brows) * TC_BK * 2;
-
+  // Setup that needs no descriptor field (barriers, TMEM, the CTA / cluster
+  // sync) runs while the dependent row -> descriptor loads are in flight: the
+  // chain costs ~1 us per launch when it is waited on first.
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);  // the owning producer's expect_tx arrival
@@ -213,8 +184,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      // warps that drain one tile (CG = 2: both CTAs' epilogues arrive on CTA 0's)
-      mbar_init(&tempty[a], (stripe ? TC_EPI_WARPS : 4) * CG);
+      // every epilogue warp of the tile's CTA(s) (CG = 2: both CTAs' epilogues
+      // arrive on CTA 0's); a warp draining a whole tile alone arrives 3x
+      mbar_init(&tempty[a], TC_EPI_WARPS * CG);
     }
     mbar_init(bfull, 1);
     for (int r = 0; r < TC_RR_SLOTS; ++r) {
@@ -222,8 +194,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&rempty[r], 4);  // the group's four warps
     }
     fence_mbar_init();
-    tma_prefetch(wm);
-    tma_prefetch(&dp->amap);
   }
   if (warp == TC_MMA_WARP) {
     if (CG == 2)
@@ -236,6 +206,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (CG == 2) cluster_sync();  // the peer's barriers exist before any remote arrival / TMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  // WeightSlice tile width of the actuated subnet (conv_bn_active); its own
+  // weight map (box = bn / CG rows) when the subnet row carries one that
+  // matches, else the graph's max-width map (extra rows land unused)
+  const int bn = (p.dbg & 4194304) ? p.bn : conv_bn_active(p.bn, d.cout, CG);  // A/B switch
+  const bool own_wmap = d_wrows == bn / CG;
+  const CUtensorMap* wm = own_wmap ? &dp->wmap : &wmap;
+  const int brows = own_wmap ? bn / CG : p.bn / CG;  // rows each B box lands
+  const int mt = (p.M + TC_BM * CG - 1) / (TC_BM * CG);  // CG = 2: 256-row pair tiles
+  const int nt = (d.cout + bn - 1) / bn;  // WeightSlice: only tiles inside cout_a
+  const int tiles = mt * nt;
+  const int S = p.splits > 1 ? p.splits : 1;  // split-K: work unit u = (tile u / S, K range u % S)
+  const int units = tiles * S;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int unit0 = static_cast<int>(blockIdx.x) / CG;     // this CTA's (pair's) first tile
+  const int ustep = static_cast<int>(gridDim.x) / CG;
+  const bool idle = unit0 >= units;  // no tile of the actuated subnet (both CTAs of a pair agree)
+  // Epilogue work split: wide tiles (>= TC_EPI_GROUPS 32-column chunks) are
+  // striped chunk-wise across all groups; narrow ones go whole to one group
+  // in turn (striping 1-2 chunks over 3 groups only adds handshakes).
+  // (a narrow ACTIVE width on a wide instance stripes too: the alternate mode
+  // needs NACC % 3 == 0, which only the 64-wide instances guarantee)
+  const bool stripe = (bn + 31) / 32 >= TC_EPI_GROUPS || C::NACC % TC_EPI_GROUPS != 0;
+  // alternate mode hands tile i to group i % 3 and accumulator i % NACC: the
+  // pair must be a function of the accumulator alone
+  static_assert(BN_MAX > 64 || C::NACC % TC_EPI_GROUPS == 0, "accumulator/group mapping");
+
+  const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
+  const int cblocks = (d.cin + TC_BK - 1) / TC_BK;
+  const int nk = ka * ka * cblocks;
+  // resident B: K blocks packed at the ACTUAL tile width (bn rows of 128 B,
+  // a multiple of the 1 KB swizzle atom), which is what resident_b() sizes
+  // against TC_RB_BYTES — a BN_MAX stride overran the region for bn < BN_MAX
+  const uint32_t rb_stride = static_cast<uint32_t>(brows) * TC_BK * 2;
+  if (tid == 0 && !idle) {
+    tma_prefetch(wm);
+    tma_prefetch(&dp->amap);
+  }
   // PDL: everything above touched only smem / TMEM / static descriptors.
   // Weights are static too: the producers issue the resident slice / the
   // first ring stages' B boxes before griddepcontrol.wait, overlapping the
@@ -247,7 +255,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const long long t_begin = prof ? clock64() : 0;
 
   constexpr int NPROD = RRING ? 2 : TC_NPROD;  // residual ring: warp 3 streams the residual
-  if (RRING && warp == TC_PROD3_WARP) {
+  if (idle) {
+    // nothing to do; fall through to the common teardown
+  } else if (RRING && warp == TC_PROD3_WARP) {
     // ============================================================ residual ring
     // Chunk c of every tile goes to group c % 3's ring (the group drains
     // its chunks in this same order), slot = that group's sequence % 2.
@@ -495,11 +505,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // Every tile is drained by all TC_EPI_GROUPS groups: group g takes the
     // 32-column chunks c = g, g + G, ... (more warps in flight per tile than
     // tempty lives in CTA 0 of a pair (its MMA warp waits on it)
+    const uint32_t tcount = stripe ? 1u : static_cast<uint32_t>(TC_EPI_GROUPS);
     auto arrive_tempty = [&](int a) {
       if (CG == 2)
-        mbar_arrive_cluster(mapa_shared(&tempty[a], 0));
+        mbar_arrive_cluster_cnt(mapa_shared(&tempty[a], 0), tcount);
       else
-        mbar_arrive(&tempty[a]);
+        mbar_arrive_cnt(&tempty[a], tcount);
     };
     // alternating whole tiles between two groups, which left the epilogue
     // latency-bound).  A group without a chunk in a tile still waits for the
