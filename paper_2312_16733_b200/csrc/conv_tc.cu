@@ -521,6 +521,143 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int t = unit0 + i * ustep;
     int c = c0;
     int rk = 0;  // RESB = 2: chunks this group has drained (residual ring sequence)
+    // TMA-store epilogue (`ys`): the descriptor row carries this subnet's
+    // output map.  Row per lane straight from tcgen05.ld (no fp32 transpose
+    // through shared memory): SubnetNorm columns by warp shuffle, the residual
+    // row as four 16-byte vectors (global or the 64B-swizzled ring slot), the
+    // bf16 chunk written once into a 64B-swizzled 2 KB box and stored by ONE
+    // TMA store.  Shared-memory traffic per chunk drops from 8 KB (fp32 STS +
+    // LDS) to 4 KB (bf16 STS + TMA read) and the per-lane STG chain goes.
+    // Needs whole 32-column chunks inside the tile (one N tile, or bn % 32 = 0).
+    const bool ys = p.ystore && S == 1 && !p.out_f32 && (d.cout & 7) == 0 &&
+                    (nt == 1 || (bn & 31) == 0) && !(p.dbg & 33554432);
+    if (ys) {
+      uint8_t* ybuf = epi_base + ew * 4096;  // two 2 KB staging boxes per warp
+      const __nv_bfloat16* resp = static_cast<const __nv_bfloat16*>(p.res);
+      int yb = 0;
+      while (t < units) {
+        int tn = t, cn = c + c_step, inx = i;
+        if (cn >= chunks_of(t)) {
+          cn = c0;
+          inx = i + i_step;
+          tn = t + i_step * ustep;
+        }
+        const bool have = c < chunks_of(t);
+        const int row0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
+        const int col0 = (t % nt) * bn + c * 32;
+        const int m = row0 + lane;
+        float scl = 1.f, shl = 0.f;  // lane j: SubnetNorm of column col0 + j
+        uint4 rv[4];
+        if (have) {
+          const int cj = col0 + lane;
+          if (d.scale) scl = cj < d.cout ? __ldg(d.scale + cj) : 0.f;
+          if (d.shift) shl = cj < d.cout ? __ldg(d.shift + cj) : 0.f;
+          if (!RRING && has_res) {
+            const __nv_bfloat16* rp = resp + static_cast<size_t>(m < p.M ? m : 0) * d.ldo + col0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              rv[q] = col0 + q * 8 < d.cout ? __ldg(reinterpret_cast<const uint4*>(rp + q * 8))
+                                            : make_uint4(0, 0, 0, 0);
+          }
+        }
+        const int a = i % NACC;
+        if (c == c0) {
+          mbar_wait(&tfull[a], static_cast<uint32_t>(i / NACC) & 1);
+          tc_fence_after();
+        }
+        if (!have) {  // no chunk of this tile for this group
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_tempty(a);
+          t = tn;
+          c = cn;
+          i = inx;
+          continue;
+        }
+        float v[32];
+        tmem_ld32(tmem + a * BN_MAX + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+        if (inx != i) {  // this warp's last chunk of the tile is out of TMEM
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_tempty(a);
+        }
+        const int sw = (lane >> 1) & 3;  // 64B swizzle: 16-B chunk q of row r sits at q ^ ((r >> 1) & 3)
+        if (RRING && has_res) {
+          const int slot = group * 2 + (rk & 1);
+          mbar_wait(&rfull[slot], static_cast<uint32_t>(rk >> 1) & 1);
+          const uint8_t* rs = sR + slot * TC_RR_SLOT + (quarter * 32 + lane) * 64;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rv[q] = *reinterpret_cast<const uint4*>(rs + ((q ^ sw) << 4));
+          fence_proxy_async_smem();  // reads ordered before the producer's next TMA write
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rempty[slot]);
+          ++rk;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          v[j] = v[j] * __shfl_sync(0xffffffffu, scl, j) + __shfl_sync(0xffffffffu, shl, j);
+        if (has_res && !res_post) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[q]);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float2 f = __bfloat1622float2(rh[h]);
+              v[q * 8 + 2 * h] += f.x;
+              v[q * 8 + 2 * h + 1] += f.y;
+            }
+          }
+        }
+        if (act == 1) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+        } else if (EPI == 1 && act == 2) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= fminf(fmaxf(v[j] + 3.f, 0.f), 6.f) * (1.f / 6.f);
+        } else if (EPI == 2 && act == 3) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_erf_fast(v[j]);
+        } else if (EPI == 2 && act) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_apply(v[j], act);
+        }
+        if (has_res && res_post) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[q]);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float2 f = __bfloat1622float2(rh[h]);
+              v[q * 8 + 2 * h] += f.x;
+              v[q * 8 + 2 * h + 1] += f.y;
+            }
+          }
+        }
+        if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
+        __syncwarp();
+        uint8_t* box = ybuf + yb * 2048;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk;
+          pk.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+          pk.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+          pk.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+          pk.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+          *reinterpret_cast<uint4*>(box + lane * 64 + ((q ^ sw) << 4)) = pk;
+        }
+        fence_proxy_async_smem();  // generic-proxy writes visible to the TMA store
+        __syncwarp();
+        if (lane == 0 && row0 < p.M && !(p.dbg & 1)) {
+          tma_store_2d(&dp->ymap, box, col0, row0);
+          bulk_commit();
+        }
+        yb ^= 1;
+        t = tn;
+        c = cn;
+        i = inx;
+      }
+      if (lane == 0) bulk_wait<0>();  // stores complete before the CTA retires
+    } else {
     EpiIn cur;  // this chunk's SubnetNorm row + residual (no register prefetch:
                 // 12 warps hide the latency, and 512 threads cap registers at 128)
     while (t < units) {
@@ -580,7 +717,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (RRING && has_res) {  // this chunk's residual rows from the group's ring slot
         const int slot = group * 2 + (rk & 1);
         mbar_wait(&rfull[slot], static_cast<uint32_t>(rk >> 1) & 1);
-        const uint8_t* rs = sR + slot * TC_RR_SLOT + (quarter * 32 + rsub) * 64 + seg * 16;
+        // rows quarter*32 + rsub + 8*r4 share (row >> 1) & 3 = (rsub >> 1) & 3 (64B swizzle)
+        const uint8_t* rs = sR + slot * TC_RR_SLOT + (quarter * 32 + rsub) * 64 + ((seg ^ ((rsub >> 1) & 3)) << 4);
 #pragma unroll
         for (int r4 = 0; r4 < 4; ++r4) cur.rv[r4] = *reinterpret_cast<const uint4*>(rs + r4 * 8 * 64);
         // generic-proxy reads ordered before the producer's next async-proxy (TMA) write
@@ -706,6 +844,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       c = cn;
       i = inx;
     }
+    }  // !ys
   } else if (warp == TC_MMA_WARP && rank == 0) {
     // ============================================================ MMA issuer
     // Converged warp, elected lane issues (tc_mma_bf16_elect); descriptors
@@ -906,8 +1045,24 @@ int make_res_map(CUtensorMap* map, const void* r, long rows, int cout, int ld) {
   cuuint32_t box[2] = {32, static_cast<cuuint32_t>(TC_BM)};
   cuuint32_t estr[2] = {1, 1};
   CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(r), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS ? 0 : -static_cast<int>(res);
+}
+
+// Output of a bf16 conv_tc op: 2-D tiled map over [rows][cout] (row pitch
+// ld), box {32 columns, 32 rows}, 64B-swizzled (the TMA-store epilogue's
+// staging layout).  Rows past `rows` and columns past `cout` are clipped.
+int make_y_map(CUtensorMap* map, void* y, long rows, int cout, int ld) {
+  static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
+  if (!enc || (cout & 7) != 0 || (ld & 7) != 0) return -1;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cout), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS ? 0 : -static_cast<int>(res);
 }
 

@@ -39,6 +39,10 @@ struct alignas(64) OpDesc {
   // box {64 ch, hrows, 3 taps} at this subnet's tile width (0 = graph map)
   CUtensorMap hmap;
   int hrows;
+  // conv_tc output as THIS subnet lays it out: 2-D tiled map over
+  // [rows][cout_a], box {32 columns, 32 rows}, 64-byte swizzle — the epilogue
+  // stores each warp's bf16 32 x 32 chunk with one TMA store
+  CUtensorMap ymap;
   // activation row strides (elements) of this op's input and output/residual
   // buffers as THIS subnet lays them out: bf16 CNN activations pad rows to 32
   // bytes (act_ld: 16-channel multiples) — 16-byte-aligned rows (widths
@@ -174,6 +178,7 @@ struct ConvParams {
   int splits;
   float* ws;
   int rres;           // the descriptor row carries rmap for this op (engine)
+  int ystore;         // conv_tc: descriptor rows carry ymap (TMA-store epilogue)
   int dbg;            // profiling knob (SSN_TC_DEBUG): 1 = epilogue skips global
                       // memory, 2 = no MMA issued (bottleneck isolation only)
   // depthwise (dw.cu): TMA stage ring, and the fused squeeze-excite pool:

@@ -37,6 +37,7 @@ int choose_bn(int cout_max, long M, int nk_max);
 bool conv_tc_use_pairs(const ConvParams& p);
 int conv_tc_splits(const ConvParams& p);
 int make_res_map(CUtensorMap* map, const void* r, long rows, int cout, int ld);
+int make_y_map(CUtensorMap* map, void* y, long rows, int cout, int ld);
 cudaError_t launch_conv_tc(const ConvParams& p, const CUtensorMap& wmap, cudaStream_t s);
 cudaError_t init_conv_tc();
 cudaError_t init_conv_halo();
@@ -389,6 +390,8 @@ static void conv_tc_tiling(const ssn_engine* e, int oi, ConvParams& p) {
   p.rres = o.res != S_NONE && (o.cout_max & 7) == 0;  // every subnet's row carries rmap
   p.splits = conv_tc_splits(p);
   p.cg2 = p.splits > 1 ? 0 : conv_tc_use_pairs(p);
+  // every subnet row of a bf16 conv carries ymap (subnet registration)
+  p.ystore = o.kind != OP_LINEAR && (o.cout_max & 7) == 0 && p.splits <= 1;
 }
 
 static int enqueue_op(ssn_engine* e, int oi, const int* map, uint32_t batch, cudaStream_t s) {
@@ -700,6 +703,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
   std::vector<const void*> in_ptr(st.plan.ops.size(), nullptr);
   std::vector<const void*> res_ptr(st.plan.ops.size(), nullptr);
   std::vector<const void*> in2_ptr(st.plan.ops.size(), nullptr), in3_ptr(st.plan.ops.size(), nullptr);
+  std::vector<const void*> out_ptr(st.plan.ops.size(), nullptr);
   bool flip = false;
   for (size_t si = 0; si < nseg; ++si) {
     st.seg_var[si] = st.seg_mask[si] | (flip ? SEG_FLIP : 0u);
@@ -711,6 +715,7 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
       res_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].res, sm.map);
       in2_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in2, sm.map);
       in3_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].in3, sm.map);
+      out_ptr[sm.op] = slot_ptr(e, e->net.ops[sm.op].out, sm.map);
     }
   }
   std::vector<OpDesc> row(st.plan.ops.size());
@@ -777,6 +782,12 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
             SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (hp) failed for op " + std::to_string(oi));
           dsc.hrows = hb / 2;
         }
+        // output map of conv_tc's TMA-store epilogue (bf16 outputs)
+        if (o.kind != OP_LINEAR && (o.cout & 7) == 0 && out_ptr[oi] &&
+            make_y_map(&dsc.ymap, const_cast<void*>(out_ptr[oi]),
+                       static_cast<long>(e->desc.max_batch) * o.hout * o.wout, o.cout,
+                       act_ld(e, o.cout)) != 0)
+          SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (output) failed for op " + std::to_string(oi));
         // residual source for conv_tc's TMA residual ring
         if (res_ptr[oi] && (o.cout & 7) == 0 &&
             make_res_map(&dsc.rmap, res_ptr[oi],
@@ -1401,6 +1412,13 @@ int ssn_op_conv_bf16(const void* x, int n, int h, int w, int cin, const void* wg
     // ragged slice, or SubnetNorm vectors the vector epilogue cannot load
     p.ragged = (cout & 7) != 0 || ((reinterpret_cast<uintptr_t>(scale) | reinterpret_cast<uintptr_t>(shift)) & 15) != 0;
     p.cg2 = conv_tc_use_pairs(p);
+    if (!out_f32 && !p.ragged) {  // TMA-store epilogue: the scratch row carries the output map
+      OpDesc d2 = d;
+      if (make_y_map(&d2.ymap, y, p.M, cout, cout) != 0)
+        SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled (output) failed");
+      p.fixed = op_desc_scratch(d2, s);
+      p.ystore = 1;
+    }
     CUtensorMap wmap{};
     if (make_weight_map(&wmap, wgt, cin_max, k * k, cout_max, p.cg2 ? p.bn / 2 : p.bn) != 0)
       SSN_THROW(SSN_E_CUDA, "cuTensorMapEncodeTiled failed");
