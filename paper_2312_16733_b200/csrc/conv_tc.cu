@@ -144,7 +144,7 @@ template <int BN_MAX, int STAGES, int KPS, int EPI, int RESB, int CG = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap wmap) {
   using C = TcCfg<BN_MAX, STAGES, KPS, RESB, CG>;
-  static_assert(CG == 1 || (RESB == 0 && KPS == 1), "2-CTA mode streams both operands");
+  static_assert(CG == 1 || RESB == 0, "2-CTA mode streams both operands");
   constexpr bool RES_B = C::RES_B;         // resident weight slice
   constexpr bool RRING = RESB >= 2;        // residual through the TMA ring
   constexpr int NACC = C::NACC;
@@ -254,7 +254,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   long long w_wait = 0, w_wait2 = 0;
   const long long t_begin = prof ? clock64() : 0;
 
-  constexpr int NPROD = RRING ? 2 : TC_NPROD;  // residual ring: warp 3 streams the residual
+  // residual ring: warp 3 streams the residual; 2-stage rings: two producers
+  constexpr int NPROD = RRING ? 2 : (STAGES < TC_NPROD ? STAGES : TC_NPROD);
   if (idle) {
     // nothing to do; fall through to the common teardown
   } else if (RRING && warp == TC_PROD3_WARP) {
@@ -316,26 +317,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // B of the first tile's leading ring stages, ahead of the PDL wait
-    const int npre = (KPS == 1 && !RES_B && !(p.dbg & 8) && S == 1) ? min(STAGES, nk) : 0;
+    // (npre STAGES; each holds KPS K blocks, the last one possibly fewer)
+    const int npre = (!RES_B && !(p.dbg & 8) && S == 1) ? min(STAGES, (nk + KPS - 1) / KPS) : 0;
     const uint32_t a_tx1 = (p.dbg & 4) ? 0u : static_cast<uint32_t>(C::A_BYTES * CG);
     const uint32_t b_tx1 = (p.dbg & 8) ? 0u : static_cast<uint32_t>(brows * CG * TC_BK * 2);
     if (npre && leader) {
       const int n0 = (unit0 % nt) * bn + static_cast<int>(rank) * (bn / CG);
       int tr = 0, ts = 0, cb = 0;
-      for (int kb = 0; kb < npre; ++kb) {
-        if (kb % NPROD == pidx) {
-          if (rank == 0) mbar_arrive_expect_tx(&full[kb], a_tx1 + b_tx1);
-          uint8_t* dst = sB + kb * C::B_BYTES;
-          if (CG == 2)
-            tma2_load_3d(dst, wm, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
-          else
-            tma_load_3d(dst, wm, &full[kb], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
-        }
-        if (++cb == cblocks) {
-          cb = 0;
-          if (++ts == ka) {
-            ts = 0;
-            ++tr;
+      for (int st = 0; st < npre; ++st) {
+        const int nsub = min(KPS, nk - st * KPS);
+        const bool mine = st % NPROD == pidx;
+        if (mine && rank == 0) mbar_arrive_expect_tx(&full[st], nsub * (a_tx1 + b_tx1));
+#pragma unroll
+        for (int j = 0; j < KPS; ++j) {
+          if (j < nsub) {
+            if (mine) {
+              uint8_t* dst = sB + (st * KPS + j) * C::B_BYTES;
+              if (CG == 2)
+                tma2_load_3d(dst, wm, &full[st], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+              else
+                tma_load_3d(dst, wm, &full[st], cb * TC_BK, (tr + koff) * p.k_max + (ts + koff), n0);
+            }
+            if (++cb == cblocks) {
+              cb = 0;
+              if (++ts == ka) {
+                ts = 0;
+                ++tr;
+              }
+            }
           }
         }
       }
@@ -1163,9 +1172,15 @@ int choose_bn(int cout_max, long M, int nk_max) {
 // Instances (BN_MAX, STAGES, K blocks per stage): the operand ring plus the
 // 36 KB epilogue staging fill the 227 KB of shared memory; resident-B
 // instances trade ring stages for the 96 KB weight block.
+// KPS = 2 instances (two K blocks per ring stage) for long-K streamed-B
+// layers: the per-stage handshake (MMA commit -> producer -> full barrier ->
+// MMA wait) costs ~520 cycles whatever the tile width (tools/ubench/
+// mma2_rate.cu: 4 MMAs per stage cap at ~131 cycles per MMA, 8 at ~85-98),
+// so a 4-MMA stage bounds every N < 256 tile below its tensor rate.
 #define SSN_TC_INSTANCES(X) X(64, 7, 1, 0, 1) X(128, 5, 1, 0, 1) X(256, 3, 1, 0, 1) \
   X(64, 4, 1, 1, 1) X(128, 4, 1, 1, 1) X(256, 4, 1, 1, 1) X(256, 5, 1, 0, 2) X(128, 7, 1, 0, 2) \
-  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2) X(256, 2, 1, 2, 1) X(192, 3, 1, 3, 1)
+  X(192, 4, 1, 0, 1) X(192, 6, 1, 0, 2) X(256, 2, 1, 2, 1) X(192, 3, 1, 3, 1) \
+  X(64, 3, 2, 0, 1) X(128, 2, 2, 0, 1) X(192, 2, 2, 0, 1) X(128, 3, 2, 0, 2) X(192, 3, 2, 0, 2)
 
 cudaError_t init_conv_tc() {
 #define SSN_TC_ATTR(BN, ST, KPS, RB, CG)                                                  \
@@ -1277,17 +1292,30 @@ cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap,
   // Resident B: the max-shape slice is one N tile (so is every subnet's) and
   // all its K blocks fit TC_RB_BYTES.
   const bool resb = resident_b(p);
-  if (p.bn <= 64) return resb ? launch_impl<64, 4, 1, 1>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
+  // two K blocks per stage on unsplit streamed-B layers with >= SSN_TC_KPS2_NK
+  // (16) K blocks
+  static const int kps2_nk = [] {
+    const char* e = getenv("SSN_TC_KPS2_NK");
+    return e ? atoi(e) : 16;
+  }();
+  const long nk_max = static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK);
+  const bool kps2 = kps2_nk > 0 && nk_max >= kps2_nk && !resb && p.splits <= 1;
+  if (p.bn <= 64) {
+    if (resb) return launch_impl<64, 4, 1, 1>(p, wmap, s);
+    return kps2 ? launch_impl<64, 3, 2, 0>(p, wmap, s) : launch_impl<64, 7, 1, 0>(p, wmap, s);
+  }
   if (p.bn <= 128) {
     if (resb) return launch_impl<128, 4, 1, 1>(p, wmap, s);
-    if (p.cg2) return launch_impl<128, 7, 1, 0, 2>(p, wmap, s);  // bn == 128 pair tiles
-    return launch_impl<128, 5, 1, 0>(p, wmap, s);
+    if (p.cg2)  // bn == 128 pair tiles
+      return kps2 ? launch_impl<128, 3, 2, 0, 2>(p, wmap, s) : launch_impl<128, 7, 1, 0, 2>(p, wmap, s);
+    return kps2 ? launch_impl<128, 2, 2, 0>(p, wmap, s) : launch_impl<128, 5, 1, 0>(p, wmap, s);
   }
   if (p.bn <= 192 && !resb && !(dbg & 524288)) {  // 144..192-wide tiles: deeper rings than BN 256
-    if (p.cg2) return launch_impl<192, 6, 1, 0, 2>(p, wmap, s);
+    if (p.cg2)
+      return kps2 ? launch_impl<192, 3, 2, 0, 2>(p, wmap, s) : launch_impl<192, 6, 1, 0, 2>(p, wmap, s);
     if (p.res && p.rres && p.splits <= 1 && !(dbg & 4194304))
       return launch_impl<192, 3, 1, 3>(p, wmap, s);  // streamed B + residual ring
-    return launch_impl<192, 4, 1, 0>(p, wmap, s);
+    return kps2 ? launch_impl<192, 2, 2, 0>(p, wmap, s) : launch_impl<192, 4, 1, 0>(p, wmap, s);
   }
   if (resb && p.res && p.rres && !(dbg & 2097152) &&
       static_cast<long>(p.k_max) * p.k_max * ((p.cin_max + TC_BK - 1) / TC_BK) * p.bn * TC_BK * 2 <=
@@ -1295,7 +1323,7 @@ cudaError_t launch_conv_tc_main(const ConvParams& p_in, const CUtensorMap& wmap,
     return launch_impl<256, 2, 1, 2>(p, wmap, s);  // residual through the TMA ring
   if (resb) return launch_impl<256, 4, 1, 1>(p, wmap, s);
   // bn > 128: pair tiles (cta_group::2) unless SSN_TC_DEBUG & 16384
-  if (p.cg2) return launch_impl<256, 5, 1, 0, 2>(p, wmap, s);
+  if (p.cg2) return launch_impl<256, 5, 1, 0, 2>(p, wmap, s);  // (a 2-stage KPS = 2 ring measured slower)
   return launch_impl<256, 3, 1, 0>(p, wmap, s);
 }
 
