@@ -58,6 +58,9 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (64, 14, 14, 1024, 1024, 360, 360, 1, 1, 0),     # 43: = case32 (aligned weights already)
     (64, 14, 14, 360, 368, 1024, 1024, 1, 1, 1),     # 44: case5 with 32-B weight rows
     (256, 14, 14, 360, 368, 360, 360, 3, 1, 0),      # 45: case26 with 32-B weight rows
+    (64, 28, 28, 360, 360, 360, 360, 3, 2, 0),       # 46: max stage-3 stride-2 3x3 (28 -> 14 px)
+    (64, 56, 56, 176, 176, 176, 176, 3, 2, 0),       # 47: max stage-2 stride-2 3x3 (56 -> 28 px)
+    (64, 14, 14, 720, 720, 720, 720, 3, 2, 0),       # 48: max stage-4 stride-2 3x3 (14 -> 7 px)
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
