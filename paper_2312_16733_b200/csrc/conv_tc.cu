@@ -63,6 +63,8 @@ constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 512
 
 constexpr int TC_STG_LD = 36;  // padded fp32 row of the 32x32 epilogue transpose tile
 constexpr int TC_STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
+// the TMA-store epilogue reuses the region: 2 x 2 KB boxes per warp + the SubnetNorm row
+static_assert(TC_EPI_WARPS * 4096 + 2048 <= TC_STG_BYTES, "TMA-store staging exceeds the epilogue region");
 
 // Resident-B mode (RESB): when the whole active weight slice is ONE N tile
 // of <= TC_RB_BYTES (narrow 1x1 convs: 88->256, 256->88, 64->256 ...), it is
@@ -538,29 +540,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // TMA store.  Shared-memory traffic per chunk drops from 8 KB (fp32 STS +
     // LDS) to 4 KB (bf16 STS + TMA read) and the per-lane STG chain goes.
     // Needs whole 32-column chunks inside the tile (one N tile, or bn % 32 = 0).
+    // (a residual from global memory keeps the coalesced path: row-per-lane
+    // 16-B residual loads measured slower on the 56-px 88->256 expand,
+    // 69 -> 78 us; SSN_TC_DEBUG & 67108864 overrides for A/B)
     const bool ys = p.ystore && S == 1 && !p.out_f32 && (d.cout & 7) == 0 &&
-                    (nt == 1 || (bn & 31) == 0) && !(p.dbg & 33554432);
+                    (nt == 1 || (bn & 31) == 0) && !(p.dbg & 33554432) &&
+                    (RRING || p.res == nullptr || (p.dbg & 67108864));
     if (ys) {
       uint8_t* ybuf = epi_base + ew * 4096;  // two 2 KB staging boxes per warp
       const __nv_bfloat16* resp = static_cast<const __nv_bfloat16*>(p.res);
       int yb = 0;
+      // One N tile (every tile has the same columns): the SubnetNorm row sits
+      // in shared memory for the whole launch (broadcast LDS.128, 16 per
+      // chunk instead of 64 shuffles) and the tile / chunk arithmetic needs
+      // no division.  ncu on the 56-px 64->256 layer: issue-bound epilogue
+      // (45% issue slots, LSU pipe 41% from the shuffles).
+      const bool one_nt = nt == 1;
+      const int nch1 = chunks_of(0);
+      float* sn = reinterpret_cast<float*>(epi_base + TC_EPI_WARPS * 4096);  // [256] scale, [256] shift
+      if (one_nt) {
+        for (int k = ew * 32 + lane; k < 512; k += TC_EPI_WARPS * 32) {
+          const int cj = k & 255;
+          const float* src = k < 256 ? d.scale : d.shift;
+          sn[k] = cj < d.cout && src ? __ldg(src + cj) : (k < 256 && !src ? 1.f : 0.f);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(TC_EPI_WARPS * 32) : "memory");  // epilogue warps only
+      }
+      const bool relu_pack = act == 1 && !(has_res && res_post);
       while (t < units) {
+        const int tm = one_nt ? t : t / nt;  // M tile
+        const int tq = t - tm * nt;          // N tile
+        const int nch = one_nt ? nch1 : chunks_of(t);
         int tn = t, cn = c + c_step, inx = i;
-        if (cn >= chunks_of(t)) {
+        if (cn >= nch) {
           cn = c0;
           inx = i + i_step;
           tn = t + i_step * ustep;
         }
-        const bool have = c < chunks_of(t);
-        const int row0 = (t / nt) * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
-        const int col0 = (t % nt) * bn + c * 32;
+        const bool have = c < nch;
+        const int row0 = tm * TC_BM * CG + static_cast<int>(rank) * TC_BM + quarter * 32;
+        const int col0 = tq * bn + c * 32;
         const int m = row0 + lane;
         float scl = 1.f, shl = 0.f;  // lane j: SubnetNorm of column col0 + j
         uint4 rv[4];
         if (have) {
-          const int cj = col0 + lane;
-          if (d.scale) scl = cj < d.cout ? __ldg(d.scale + cj) : 0.f;
-          if (d.shift) shl = cj < d.cout ? __ldg(d.shift + cj) : 0.f;
+          if (!one_nt) {
+            const int cj = col0 + lane;
+            if (d.scale) scl = cj < d.cout ? __ldg(d.scale + cj) : 0.f;
+            if (d.shift) shl = cj < d.cout ? __ldg(d.shift + cj) : 0.f;
+          }
           if (!RRING && has_res) {
             const __nv_bfloat16* rp = resp + static_cast<size_t>(m < p.M ? m : 0) * d.ldo + col0;
 #pragma unroll
@@ -602,9 +630,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (lane == 0) mbar_arrive(&rempty[slot]);
           ++rk;
         }
+        if (one_nt) {
+          const float4* s4 = reinterpret_cast<const float4*>(sn + c * 32);
+          const float4* h4 = reinterpret_cast<const float4*>(sn + 256 + c * 32);
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          v[j] = v[j] * __shfl_sync(0xffffffffu, scl, j) + __shfl_sync(0xffffffffu, shl, j);
+          for (int j = 0; j < 8; ++j) {
+            const float4 sc = s4[j], sh = h4[j];
+            v[4 * j] = v[4 * j] * sc.x + sh.x;
+            v[4 * j + 1] = v[4 * j + 1] * sc.y + sh.y;
+            v[4 * j + 2] = v[4 * j + 2] * sc.z + sh.z;
+            v[4 * j + 3] = v[4 * j + 3] * sc.w + sh.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            v[j] = v[j] * __shfl_sync(0xffffffffu, scl, j) + __shfl_sync(0xffffffffu, shl, j);
+        }
         if (has_res && !res_post) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -617,7 +658,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
         }
-        if (act == 1) {
+        if (act == 1 && !relu_pack) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
         } else if (EPI == 1 && act == 2) {
@@ -648,10 +689,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 pk;
-          pk.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-          pk.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-          pk.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-          pk.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+          if (relu_pack) {
+            pk.x = pack_bf16x2_relu(v[q * 8 + 0], v[q * 8 + 1]);
+            pk.y = pack_bf16x2_relu(v[q * 8 + 2], v[q * 8 + 3]);
+            pk.z = pack_bf16x2_relu(v[q * 8 + 4], v[q * 8 + 5]);
+            pk.w = pack_bf16x2_relu(v[q * 8 + 6], v[q * 8 + 7]);
+          } else {
+            pk.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+            pk.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+            pk.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+            pk.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+          }
           *reinterpret_cast<uint4*>(box + lane * 64 + ((q ^ sw) << 4)) = pk;
         }
         fence_proxy_async_smem();  // generic-proxy writes visible to the TMA store

@@ -648,6 +648,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// bf16x2 {lo = relu(a), hi = relu(b)} in one cvt (ReLU fused into the rounding)
+__device__ __forceinline__ uint32_t pack_bf16x2_relu(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
 
 #ifdef __CUDACC__
 // Host: launch `k` with programmatic stream serialization (PDL; graph capture

@@ -61,6 +61,7 @@ CASES = [  # n, h, w, cin, cin_max, cout, cout_max, k, stride, residual
     (64, 28, 28, 360, 360, 360, 360, 3, 2, 0),       # 46: max stage-3 stride-2 3x3 (28 -> 14 px)
     (64, 56, 56, 176, 176, 176, 176, 3, 2, 0),       # 47: max stage-2 stride-2 3x3 (56 -> 28 px)
     (64, 14, 14, 720, 720, 720, 720, 3, 2, 0),       # 48: max stage-4 stride-2 3x3 (14 -> 7 px)
+    (64, 56, 56, 64, 64, 256, 256, 1, 1, 0),         # 49: max stage-1 downsample / expand-sized 1x1 (HBM-bound)
 ]
 only = os.environ.get("CASES")
 for ci, c in enumerate(CASES):
