@@ -555,7 +555,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // chunk instead of 64 shuffles) and the tile / chunk arithmetic needs
       // no division.  ncu on the 56-px 64->256 layer: issue-bound epilogue
       // (45% issue slots, LSU pipe 41% from the shuffles).
-      const bool one_nt = nt == 1;
+      // (not in the GELU / ragged instance: its SASS is the largest and the
+      // extra path cost BERT's FFN-up 8% through instruction-cache misses)
+      const bool one_nt = EPI != 2 && nt == 1 && !(p.dbg & 134217728);  // (A/B: shuffle path)
       const int nch1 = chunks_of(0);
       float* sn = reinterpret_cast<float*>(epi_base + TC_EPI_WARPS * 4096);  // [256] scale, [256] shift
       if (one_nt) {
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         asm volatile("bar.sync 1, %0;" ::"r"(TC_EPI_WARPS * 32) : "memory");  // epilogue warps only
       }
-      const bool relu_pack = act == 1 && !(has_res && res_post);
+      const bool relu_pack = EPI == 0 && act == 1 && !(has_res && res_post);
       while (t < units) {
         const int tm = one_nt ? t : t / nt;  // M tile
         const int tq = t - tm * nt;          // N tile
