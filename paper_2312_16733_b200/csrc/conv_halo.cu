@@ -49,12 +49,43 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
 
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
+  const int d_wrows = dp->wrows;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = bars;                         // [HL_MAX_STAGES]
+  uint64_t* empty = full + HL_MAX_STAGES;
+  uint64_t* tfull = empty + HL_MAX_STAGES;       // [4]
+  uint64_t* tempty = tfull + 4;                  // [4]
+  uint64_t* bfull = tempty + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 2);
+  // barriers and TMEM need no descriptor field: they run while the row ->
+  // descriptor loads are in flight (as conv_tc)
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp index through shfl: the compiler then knows it is warp-uniform, so
+  // role branches stay uniform and MMA/TMA operands live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  if (tid == 0) {
+    for (int s = 0; s < HL_MAX_STAGES; ++s) {  // (ST is descriptor-dependent)
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 4; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // the owning group's warps
+    }
+    mbar_init(bfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == HL_MMA_WARP) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
   const int ka = d.k, pad = d.pad, koff = (p.k_max - ka) / 2;
   const HaloGeom hg = halo_geom(p.w_, ka);
   const int wp = hg.wp, rt = hg.rt, R = hg.r;
   const int tpi = (p.h + rt - 1) / rt;  // tiles per image
   const int tiles = p.n * tpi;
-  if (static_cast<int>(blockIdx.x) >= tiles) return;
+  const bool idle = static_cast<int>(blockIdx.x) >= tiles;
   const int cin16 = (d.cin + 15) & ~15;
   const int ncb = (cin16 + HL_CB - 1) / HL_CB;
   const int bn = (d.cout + 15) & ~15;  // MMA N: the whole active cout (<= 128)
@@ -77,7 +108,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   // memory a narrow subnet leaves free deepens the window ring (e.g. OFA-R50
   // mid at 56 px: 74 of the max shape's 166 KB, 3 -> 8 stages).  A row
   // without one (operator API) uses the graph's max-width map.
-  const bool own_b = dp->wrows == bn;
+  const bool own_b = d_wrows == bn;
   const CUtensorMap* wm = own_b ? &dp->wmap : &wmap;
   const int ncb_b = own_b ? ncb : p.hb_chunks;                          // resident 32-ch blocks
   const uint32_t b_blk = static_cast<uint32_t>(own_b ? bn : p.hb_rows) * 64;  // one (tap, cb) block
@@ -85,13 +116,6 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   const uint32_t a_box = static_cast<uint32_t>(R * wp) * 64;           // TMA box bytes
   const uint32_t a_stage = (a_box + 1023) & ~1023u;                    // swizzle-atom aligned
   // [barriers + SubnetNorm vectors: 2 KB][resident B][A ring]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* full = bars;                         // [HL_MAX_STAGES]
-  uint64_t* empty = full + HL_MAX_STAGES;
-  uint64_t* tfull = empty + HL_MAX_STAGES;       // [4]
-  uint64_t* tempty = tfull + 4;                  // [4]
-  uint64_t* bfull = tempty + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 2);
   // SubnetNorm scale / shift of this op (cout <= 128), staged once: the
   // row-per-lane epilogue reads all columns per lane, and per-column global
   // loads issued right before their FMAs serialised an L1/L2 round trip per
@@ -102,30 +126,11 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
   int ST = static_cast<int>((static_cast<uint32_t>(p.h_smem) - 2048u - ((b_bytes + 1023) & ~1023u)) /
                             a_stage);
   ST = ST > HL_MAX_STAGES ? HL_MAX_STAGES : ST;
-
-  const int tid = threadIdx.x, lane = tid & 31;
-  // warp index through shfl: the compiler then knows it is warp-uniform, so
-  // role branches stay uniform and MMA/TMA operands live in uniform registers
-  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  if (tid == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 4; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // the owning group's warps
-    }
-    mbar_init(bfull, 1);
-    fence_mbar_init();
+  if (tid == 0 && !idle) {
     tma_prefetch(wm);
     tma_prefetch(&dp->amap);
   }
-  if (warp == HL_MMA_WARP) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+
   // PDL: the resident weights are static and load before griddepcontrol.wait
   // (overlapping the predecessor's tail); activations only after it
   pdl_trigger();
@@ -142,7 +147,9 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     mbar_wait(bar, ph);                       \
   }
 
-  if (warp == 0) {
+  if (idle) {
+    // no tile for this CTA: straight to the teardown
+  } else if (warp == 0) {
     // ============================================================ producer
     const bool leader = elect_one();
     if (leader && (p.dbg & 8)) {  // profiling: no weight load

@@ -84,23 +84,12 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
 
   const OpDesc* dp = desc_ptr(p.row, p.fixed, p.op);
   const OpDims d = load_desc(p.row, p.fixed, p.op);
-  const int bn = conv_bn_active(p.bn, d.cout, 2);
-  // the subnet row's hmap has this subnet's tile width; a row without one
-  // uses the graph's max-width map (rows past the active width land unused)
-  const bool own_wmap = dp->hrows == bn / 2;
-  const CUtensorMap* wm = own_wmap ? &dp->hmap : &wmap;
-  const int brows = own_wmap ? bn / 2 : p.bn / 2;
-  const int nt = (d.cout + bn - 1) / bn;
-  const int tpi = (p.h + rt - 1) / rt;           // CTA tiles per image
-  const int pairs = (p.n * tpi + 1) / 2;          // pair tiles (2 CTA tiles each)
-  const int units = pairs * nt;
-  const uint32_t rank = cluster_rank();
-  const int u0 = static_cast<int>(blockIdx.x) / 2, ustep = static_cast<int>(gridDim.x) / 2;
-  if (u0 >= units) return;  // both CTAs of a pair agree
-  const int ncb = (d.cin + 63) / 64;
+  const int d_hrows = dp->hrows;
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
 
+  // barriers, TMEM and the cluster sync need no descriptor field: they run
+  // while the row -> descriptor loads are in flight (as conv_tc)
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], 1);
@@ -115,8 +104,6 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
       mbar_init(&tempty[a], HP_EPI_WARPS * 2);  // both CTAs' epilogue warps
     }
     fence_mbar_init();
-    tma_prefetch(wm);
-    tma_prefetch(&dp->rmap);
   }
   if (warp == 1) tmem2_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -124,6 +111,25 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  const int bn = conv_bn_active(p.bn, d.cout, 2);
+  // the subnet row's hmap has this subnet's tile width; a row without one
+  // uses the graph's max-width map (rows past the active width land unused)
+  const bool own_wmap = d_hrows == bn / 2;
+  const CUtensorMap* wm = own_wmap ? &dp->hmap : &wmap;
+  const int brows = own_wmap ? bn / 2 : p.bn / 2;
+  const int nt = (d.cout + bn - 1) / bn;
+  const int tpi = (p.h + rt - 1) / rt;           // CTA tiles per image
+  const int pairs = (p.n * tpi + 1) / 2;          // pair tiles (2 CTA tiles each)
+  const int units = pairs * nt;
+  const uint32_t rank = cluster_rank();
+  const int u0 = static_cast<int>(blockIdx.x) / 2, ustep = static_cast<int>(gridDim.x) / 2;
+  const bool idle = u0 >= units;  // both CTAs of a pair agree
+  const int ncb = (d.cin + 63) / 64;
+  if (tid == 0 && !idle) {
+    tma_prefetch(wm);
+    tma_prefetch(&dp->rmap);
+  }
   pdl_trigger();
 
   // CTA tile q -> (image, first output row); tile index past the batch = idle half
@@ -133,7 +139,9 @@ __global__ void __launch_bounds__(HP_THREADS, 1)
     r0 = (q - img * tpi) * rt;
   };
 
-  if (warp == 0) {
+  if (idle) {
+    // no pair tile of the actuated subnet: straight to the teardown
+  } else if (warp == 0) {
     // ====================================================== window producer
     const bool leader = elect_one();
     pdl_wait();
