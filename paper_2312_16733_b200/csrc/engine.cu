@@ -272,21 +272,23 @@ static void* slot_ptr(ssn_engine* e, int slot, const int* map) {
 // Row stride (elements) of a `c`-channel activation buffer.  Every kernel of
 // the bf16 CNN path addresses activations through the descriptor row's
 // ldi / ldo and every TMA map takes the stride separately, so rows can be
-// padded.  SSN_PAD_ROWS=1 pads bf16 CNN rows to 16-channel multiples (32-B
-// rows; OFA widths are make_divisible(., 8), so 88, 360, 56, 104, 408, 136,
-// ... have 16-byte-aligned rows, which slowed conv_tc's im2col reads by up
-// to 1.6x in isolation, profiles/round2/align_probe_*).  Measured on the
-// networks it is a wash (R50 bs64 sweep 4052 -> 4050 us, bs256 max -3%;
-// OFA-MBv3 +1-4% from the extra bytes of 72/136/408-wide layers now that the
-// wide 14/28-px 3x3 convs read tiled windows), so rows stay compact by
-// default.  Pad channels are never read as data: TMA maps bound the channel
-// dimension at the active width, the vector epilogues touch c columns.
+// padded to 16-channel multiples (32-B rows) once they are >= 256 channels
+// wide.  OFA widths are make_divisible(., 8), so 360, 408, 264, 664, 1640 ...
+// have rows aligned to 16 B only, and TMA reads such rows at about half rate
+// whatever the box mode (tools/ubench/tma_modes.cu: a 3x3 A operand over
+// 360-channel pixels 32 B/cycle/SM, over 368 or 384 channels 52-72); below
+// 256 channels the layers are HBM-bound and the extra bytes cost more than
+// the faster reads return (padding every row measured -0.8% on the R50
+// sweep, >= 256 only +0.7%; OFA-MBv3 unchanged).  SSN_PAD_ROWS = t sets the
+// threshold (1 = every row, 0 = compact rows).  Pad channels are never read
+// as data: TMA maps bound the channel dimension at the active width, the
+// vector epilogues touch c columns.
 static int act_ld(const ssn_engine* e, int c) {
-  static const bool pad = [] {
+  static const int pad_min = [] {
     const char* v = getenv("SSN_PAD_ROWS");
-    return v && atoi(v) != 0;
+    return v ? atoi(v) : 256;
   }();
-  if (!pad || !e->bf16 || e->desc.family == SSN_FAMILY_BERT || c < 16) return c;
+  if (pad_min <= 0 || !e->bf16 || e->desc.family == SSN_FAMILY_BERT || c < 16 || c < pad_min) return c;
   return (c + 15) & ~15;
 }
 

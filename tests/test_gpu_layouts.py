@@ -1,8 +1,9 @@
 """Storage-layout switches, each in a fresh process (the engine reads them once):
 
-* SSN_PAD_ROWS=1   — bf16 CNN activation rows padded to 16-channel multiples,
-                     every kernel addressing activations through the descriptor
-                     row's ldi / ldo (engine.cu act_ld);
+* SSN_PAD_ROWS=1 / 0 — every bf16 CNN activation row padded to a 16-channel
+                     multiple / none (the default pads rows of >= 256
+                     channels); every kernel addresses activations through
+                     the descriptor row's ldi / ldo (engine.cu act_ld);
 * SSN_PACK_WEIGHTS=1 — compact weight rows instead of the default 32-B rows
                      (supernet.hpp Builder::pad16).
 
@@ -46,11 +47,12 @@ print("REL", worst)
 """
 
 
-@pytest.mark.parametrize("env", ["SSN_PAD_ROWS", "SSN_PACK_WEIGHTS"])
-def test_layout_switch_keeps_parity(gpu, env):
+@pytest.mark.parametrize("env,val", [("SSN_PAD_ROWS", "1"), ("SSN_PAD_ROWS", "0"),
+                                     ("SSN_PACK_WEIGHTS", "1")])
+def test_layout_switch_keeps_parity(gpu, env, val):
     out = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)], cwd=ROOT,
-                         env={**os.environ, env: "1"}, capture_output=True, text=True, timeout=600)
+                         env={**os.environ, env: val}, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     rel = float([l for l in out.stdout.splitlines() if l.startswith("REL")][-1].split()[1])
-    print(f"{env}=1: worst rel L2 vs bf16-storage oracle {rel:.2e}")
+    print(f"{env}={val}: worst rel L2 vs bf16-storage oracle {rel:.2e}")
     assert rel <= 2e-2
