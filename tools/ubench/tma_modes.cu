@@ -3,7 +3,8 @@
 // px stride-2 layer of OFA-ResNet50 (input [64][28][28][360] bf16, 36 MB,
 // L2-resident after the first pass).  Every CTA (one per SM) streams 16 KB
 // A boxes of (tap, 64-channel block, pixel tile) through a 6-deep ring with
-// 3 producer threads (as conv_tc); reports B/cycle/SM of the slowest SM.
+// P producer threads (argv[2], default 3 as conv_tc); reports B/cycle/SM of
+// the slowest SM.
 //   mode 0: im2col, stride 2 (conv_tc today): 128 output pixels per box
 //   mode 1: tiled, element strides {1, 2, 2, 1}: 14 x 9 output pixels of one
 //           image per box (126 rows)
@@ -17,11 +18,11 @@
 #include "device.cuh"
 using namespace ssn;
 
-constexpr int N = 64, H = 28, W = 28, STAGES = 6, P = 3;
+constexpr int N = 64, H = 28, W = 28, STAGES = 6;
 static int C = 360;  // argv[1]: channels = pixel pitch / 2 (360: 720-B rows, 16-B aligned only)
 
 __global__ void __launch_bounds__(256, 1) k(const __grid_constant__ CUtensorMap map, int mode, int iters,
-                                          long long* out) {
+                                          long long* out, int P) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* buf = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
   __shared__ uint64_t full[STAGES], empty[STAGES];
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(256, 1) k(const __grid_constant__ CUtensorMap 
 
 int main(int argc, char** argv) {
   if (argc > 1) C = atoi(argv[1]);
+  const int P = argc > 2 ? atoi(argv[2]) : 3;  // producer warps (<= STAGES, <= 7)
   void* src;
   const size_t bytes = static_cast<size_t>(N) * H * W * C * 2;
   cudaMalloc(&src, bytes);
@@ -113,14 +115,14 @@ int main(int argc, char** argv) {
       continue;
     }
     const int iters = 3000;
-    for (int rep = 0; rep < 2; ++rep) k<<<148, 256, smem>>>(m, mode, iters, d);
+    for (int rep = 0; rep < 2; ++rep) k<<<148, 256, smem>>>(m, mode, iters, d, P);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[148];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     double mx = 0;
     for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
     const double b = mode == 1 || mode == 3 ? 126 * 128 : 128 * 128;
-    printf("C %d mode %d (%s, stride %u): %6.1f B/cycle/SM  %s\n", C, mode,
+    printf("C %d P %d mode %d (%s, stride %u): %6.1f B/cycle/SM  %s\n", C, P, mode,
            mode == 0 || mode == 2 ? "im2col" : "tiled ", st, iters * b / mx, cudaGetErrorString(e));
   }
   return 0;
