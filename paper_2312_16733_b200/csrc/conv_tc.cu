@@ -23,14 +23,17 @@
 //    descriptors stay warp-uniform (a lane-0-only loop wrapped every
 //    UTCHMMA/UTMALDG in a divergent R2UR waterfall: 500 vs 360 cycles per
 //    K block measured, tools/ubench/tc_loop.cu).
-//  * A ring stage holds KPS K blocks (the per-stage mbarrier wait + commit
-//    costs ~150-250 cycles, as much as four N=96 MMAs).
+//  * A ring stage holds KPS K blocks: one stage = one commit -> producer ->
+//    full-barrier -> MMA round trip, ~520 cycles whatever N (tools/ubench/
+//    mma2_rate.cu), so long-K layers take two K blocks per stage.
 //  * Accumulators live in a TMEM ring (NACC buffers of BN_MAX fp32 columns),
 //    so several tiles are in flight between MMA and epilogue.
-//  * Epilogue: three groups of 4 warps stripe every tile's 32-column chunks; each warp
-//    tcgen05.ld's 32 TMEM lanes x 32 columns, transposes through padded smem,
-//    then applies SubnetNorm scale/shift, residual and the activation on
-//    coalesced 64-byte row segments and stores bf16 (or fp32 logits).
+//  * Epilogue: three groups of 4 warps stripe every tile's 32-column chunks;
+//    each warp tcgen05.ld's 32 TMEM lanes x 32 columns.  Default: row per
+//    lane, SubnetNorm / residual / activation in registers, the bf16 chunk
+//    written once into a 64B-swizzled box and stored by one TMA store
+//    (OpDesc.ymap).  Split-K partials, fp32 logits, ragged widths and global
+//    residuals: transpose through padded smem, coalesced 64-byte row segments.
 //  * Subnet extents (cin_a, cout_a, k_a, SubnetNorm row, activation map) come
 //    from the actuated subnet's descriptor, so one graph-captured launch
 //    serves every subnet; the tile count follows cout_a on the device.
