@@ -354,34 +354,41 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 // chunk), 8 channel groups x 32 pixel lanes and a shared-memory reduction,
 // so the hw loads of a channel group are in flight together (one thread per
 // channel group summing hw pixels serially was latency-bound).
+// Global average pool: block = (image, 256 channels); thread = 8 channels of
+// every 8th pixel (independent 16-byte loads, ~hw/8 per thread), then an
+// 8-way smem reduction.  (One 64-channel block per CTA with 32 pixel lanes
+// left most of the 7-px kernel's time in launch / reduction latency.)
 __global__ void __launch_bounds__(256) gap_bf16_kernel(PoolParams p) {
   pdl_wait();
   pdl_trigger();
   const OpDims d = load_desc(p.row, nullptr, p.op);
   const int C = d.cin;
-  const int n = blockIdx.x, c0 = blockIdx.y * 64;
+  const int n = blockIdx.x, c0 = blockIdx.y * 256;
   if (c0 >= C) return;
   const int hw = p.h * p.w;
-  const int g = threadIdx.x & 7, lane = threadIdx.x >> 3;
+  const int g = threadIdx.x & 31, lane = threadIdx.x >> 5;
   const int c = c0 + g * 8;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(p.x) + static_cast<long>(n) * hw * d.ldi;
   if (c < C) {
-    for (int q = lane; q < hw; q += 32) {
+#pragma unroll 4
+    for (int q = lane; q < hw; q += 8) {
       float f[8];
       bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(q) * d.ldi + c)), f);
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] += f[t];
     }
   }
-  __shared__ float red[32][65];
+  __shared__ float red[8][257];
 #pragma unroll
   for (int t = 0; t < 8; ++t) red[lane][g * 8 + t] = acc[t];
   __syncthreads();
-  if (threadIdx.x < 64 && c0 + threadIdx.x < C) {
+  const int cc = c0 + threadIdx.x;
+  if (cc < C) {
     float sum = 0.f;
-    for (int l = 0; l < 32; ++l) sum += red[l][threadIdx.x];
-    static_cast<__nv_bfloat16*>(p.y)[static_cast<long>(n) * d.ldo + c0 + threadIdx.x] =
+#pragma unroll
+    for (int l = 0; l < 8; ++l) sum += red[l][threadIdx.x];
+    static_cast<__nv_bfloat16*>(p.y)[static_cast<long>(n) * d.ldo + cc] =
         __float2bfloat16_rn(sum / static_cast<float>(hw));
   }
 }
@@ -831,7 +838,7 @@ cudaError_t launch_pool(const PoolParams& p, int max_c, bool bf16, cudaStream_t 
   const dim3 rows_grid(static_cast<unsigned>((p.wo * (max_c / 8) + 255) / 256),
                        static_cast<unsigned>(p.n * p.ho));
   if (bf16 && p.kind == 4)
-    return launch_pdl(gap_bf16_kernel, dim3(p.n, (max_c + 63) / 64), dim3(256), 0, s, 1, p);
+    return launch_pdl(gap_bf16_kernel, dim3(p.n, (max_c + 255) / 256), dim3(256), 0, s, 1, p);
   if (bf16 && p.kind == 2 && p.k == 3)
     return launch_pdl(pool_k_bf16_kernel<3, 2>, rows_grid, dim3(256), 0, s, 1, p);
   if (bf16 && p.kind == 3 && p.k == 2)
