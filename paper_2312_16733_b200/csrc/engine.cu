@@ -168,6 +168,12 @@ struct ssn_engine {
   int se_cmax = 0;
   std::vector<uint32_t> grid;
   std::map<uint64_t, std::pair<cudaGraphExec_t, int>> graphs;  // key -> (exec, kernels)
+  // Whole-forward graphs: every running segment of one LayerSelect variant
+  // vector captured back to back at one batch, so the programmatic (PDL)
+  // edges continue across segment boundaries (separately launched segment
+  // graphs drain at each boundary).  key = (per-segment variant | not-run,
+  // batch); shared by every registered subnet with the same variant vector.
+  std::map<std::vector<uint32_t>, std::pair<cudaGraphExec_t, int>> fgraphs;
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;
   // Cross-stream ordering: forwards share engine state (the active-row word,
@@ -655,6 +661,47 @@ static void build_graph(ssn_engine* e, int seg, uint32_t mask, uint32_t batch) {
   e->graphs[graph_key(seg, mask, batch)] = {ex, kernels};
 }
 
+static bool fwd_graphs_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SSN_NO_FWD_GRAPH");
+    return !(v && atoi(v) != 0);
+  }();
+  return on;
+}
+
+static std::vector<uint32_t> fgraph_key(const SubnetState& sub, uint32_t batch) {
+  std::vector<uint32_t> k(sub.seg_var.size() + 1);
+  for (size_t si = 0; si < sub.seg_var.size(); ++si) k[si] = sub.seg_run[si] ? sub.seg_var[si] : 0xFFFFFFFFu;
+  k.back() = batch;
+  return k;
+}
+
+// Capture the whole forward of `sub`'s variant vector at `batch` (once per key).
+static void build_fwd_graph(ssn_engine* e, const SubnetState& sub, uint32_t batch) {
+  const std::vector<uint32_t> key = fgraph_key(sub, batch);
+  if (e->fgraphs.count(key)) return;
+  int kernels = 0;
+  CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (size_t si = 0; si < e->net.segments.size(); ++si)
+      if (sub.seg_run[si])
+        kernels += enqueue_segment(e, static_cast<int>(si), sub.seg_var[si], batch, e->cap_stream,
+                                   [](int, bool) {});
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(e->cap_stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamEndCapture(e->cap_stream, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(err);
+  e->fgraphs[key] = {ex, kernels};
+}
+
 static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
                             const float* mean, const float* var) {
   if (!c) SSN_THROW(SSN_E_INVALID, "null subnet config");
@@ -828,6 +875,8 @@ static void register_subnet(ssn_engine* e, uint32_t id, const ssn_subnet_cfg* c,
     if (e->active == static_cast<int>(id)) e->dirty = true;
   }
   e->subs[id] = std::move(st);
+  if (e->prepared && fwd_graphs_enabled())
+    for (uint32_t b : e->grid) build_fwd_graph(e, e->subs[id], b);
 }
 
 // ---------------------------------------------------------------------------
@@ -989,6 +1038,7 @@ void ssn_destroy(ssn_engine* e) {
   cudaSetDevice(e->device);
   cudaDeviceSynchronize();
   for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second.first);
+  for (auto& kv : e->fgraphs) cudaGraphExecDestroy(kv.second.first);
   for (auto& s : e->subs) {
     cudaFree(s.d_row);
     cudaFree(s.d_norm);
@@ -1076,6 +1126,10 @@ int ssn_prepare(ssn_engine* e, const uint32_t* batch_grid, uint32_t n) {
       e->grid.push_back(b);
     }
     std::sort(e->grid.begin(), e->grid.end());
+    if (fwd_graphs_enabled())
+      for (const SubnetState& sub : e->subs)
+        if (sub.ok)
+          for (uint32_t b : e->grid) build_fwd_graph(e, sub, b);
     e->prepared = true;
   });
 }
@@ -1139,13 +1193,21 @@ int ssn_forward(ssn_engine* e, const void* x, uint32_t count, uint32_t profiled_
         CUDA_TRY(cudaMemcpyAsync(e->d_raw, x, bytes, cudaMemcpyDefault, s));
       }
     }
-    for (size_t si = 0; si < e->net.segments.size(); ++si) {
-      if (!sub.seg_run[si]) continue;  // every block skipped: input passes through
-      auto it = e->graphs.find(graph_key(static_cast<int>(si), sub.seg_var[si], profiled_batch));
-      if (it == e->graphs.end()) SSN_THROW(SSN_E_STATE, "missing graph segment");
-      CUDA_TRY(cudaGraphLaunch(it->second.first, s));
-      kernels += static_cast<uint32_t>(it->second.second);
+    const auto fit = fwd_graphs_enabled() ? e->fgraphs.find(fgraph_key(sub, profiled_batch))
+                                          : e->fgraphs.end();
+    if (fit != e->fgraphs.end()) {
+      CUDA_TRY(cudaGraphLaunch(fit->second.first, s));
+      kernels += static_cast<uint32_t>(fit->second.second);
       ++graphs;
+    } else {
+      for (size_t si = 0; si < e->net.segments.size(); ++si) {
+        if (!sub.seg_run[si]) continue;  // every block skipped: input passes through
+        auto it = e->graphs.find(graph_key(static_cast<int>(si), sub.seg_var[si], profiled_batch));
+        if (it == e->graphs.end()) SSN_THROW(SSN_E_STATE, "missing graph segment");
+        CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+        kernels += static_cast<uint32_t>(it->second.second);
+        ++graphs;
+      }
     }
     if (logits)
       CUDA_TRY(cudaMemcpyAsync(logits, e->d_logits,

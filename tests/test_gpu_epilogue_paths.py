@@ -1,4 +1,4 @@
-"""conv_tc's alternative code paths compute the SAME bits:
+"""Alternative code paths compute the SAME bits:
 
 * the TMA-store epilogue (default) vs the padded-fp32-transpose epilogue
   (SSN_TC_DEBUG=33554432): identical per-element math (SubnetNorm FMA,
@@ -7,7 +7,10 @@
 * two K blocks per ring stage (default, >= 16 K blocks) vs one
   (SSN_TC_KPS2_NK=0): the MMAs accumulate the K blocks in the same order;
 * the SubnetNorm row staged in shared memory vs warp shuffles
-  (SSN_TC_DEBUG=134217728).
+  (SSN_TC_DEBUG=134217728);
+* one whole-forward CUDA graph per LayerSelect variant vector (default) vs
+  one graph per segment (SSN_NO_FWD_GRAPH=1): the same kernels in the same
+  order.
 
 Each setting runs in a fresh process (the engine reads the switches once):
 OFA-ResNet50 mid at 64 px bs16 (stage 1-4 1x1 / 3x3 convs, residual ring),
@@ -62,6 +65,7 @@ def default_logits(gpu, tmp_path_factory):
     ("transpose_epilogue", {"SSN_TC_DEBUG": "33554432"}),
     ("one_k_block_per_stage", {"SSN_TC_KPS2_NK": "0"}),
     ("shuffled_subnetnorm", {"SSN_TC_DEBUG": "134217728"}),
+    ("segment_graphs", {"SSN_NO_FWD_GRAPH": "1"}),
 ])
 def test_conv_tc_paths_bitwise_equal(default_logits, tmp_path, tag, env):
     base = default_logits
