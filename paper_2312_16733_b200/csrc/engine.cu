@@ -678,8 +678,14 @@ static std::vector<uint32_t> fgraph_key(const SubnetState& sub, uint32_t batch) 
 
 // Capture the whole forward of `sub`'s variant vector at `batch` (once per key).
 static void build_fwd_graph(ssn_engine* e, const SubnetState& sub, uint32_t batch) {
+  // bounded: an engine with hundreds of registered variant vectors keeps the
+  // per-segment graphs for the rest (SSN_FWD_GRAPH_MAX, default 256)
+  static const size_t cap = [] {
+    const char* v = getenv("SSN_FWD_GRAPH_MAX");
+    return v ? static_cast<size_t>(atol(v)) : static_cast<size_t>(256);
+  }();
   const std::vector<uint32_t> key = fgraph_key(sub, batch);
-  if (e->fgraphs.count(key)) return;
+  if (e->fgraphs.count(key) || e->fgraphs.size() >= cap) return;
   int kernels = 0;
   CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
   try {
