@@ -85,8 +85,9 @@ class ClockSampler:
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
-        self.rows = []
+        self.rows = []  # (time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -96,13 +97,29 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a few hundred ms for its first sample, longer
+            # than a short timed region: wait for it, then mark the region
+            deadline = time.time() + 5.0
+            while not self.rows and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def start(self):  # the timed region begins / ends (host clock)
+        self.t0 = time.time()
+
+    def stop(self):
+        self.t1 = time.time()
+        # one more sample after the region ends, so a region shorter than the
+        # 50 ms sampling period is bracketed by samples on both sides
+        deadline = self.t1 + 0.5
+        while self.proc and time.time() < deadline and not any(t >= self.t1 for t, _ in self.rows):
+            time.sleep(0.01)
 
     def __exit__(self, *a):
         if self.proc:
@@ -116,7 +133,18 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows, bracket = self.rows, False
+        if self.t0 is not None and self.t1 is not None:
+            inside = [r for t, r in self.rows if self.t0 <= t <= self.t1]
+            if inside:
+                rows = inside
+            else:  # region shorter than the sampling period: the samples either side
+                before = [r for t, r in self.rows if t < self.t0][-1:]
+                after = [r for t, r in self.rows if t > self.t1][:1]
+                rows, bracket = before + after, True
+        else:
+            rows = [r for _, r in self.rows]
+        for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = max(mx, float(r[2]))
@@ -127,8 +155,11 @@ class ClockSampler:
                 pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if bracket:
+            out["samples_bracket_region"] = True
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -291,12 +322,14 @@ def run_ours(args, rank, world, local_rank):
             counts["kernels"] += eng.stats()["last_forward_kernels"]
 
     # ---- device-resident timed region
-    for i in range(args.warmup):
-        step(i)
-    counts["kernels"] = 0
     with ClockSampler(local_rank) as clk:
+        for i in range(args.warmup):  # (after the sampler's first sample: the GPU is busy again)
+            step(i)
+        counts["kernels"] = 0
+        clk.start()
         _, ms = timed_region(step, args.steps, 0, CudaTimer(torch, stream),
                              sync=torch.cuda.synchronize)
+        clk.stop()
     launches = counts["kernels"]
     imgs_per_rank = args.steps * len(SUBNETS) * B
     value = world * imgs_per_rank / (ms / 1000.0)
